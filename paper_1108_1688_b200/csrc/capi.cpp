@@ -1,0 +1,731 @@
+// capi.cpp — the extern "C" boundary (include/hjmsv_b200.h): solver handles,
+// device memory, the step loop (direct launches or one captured CUDA graph per
+// full march), status conversion back to the reference's error messages, and
+// the multi-GPU batch driver (caplet_ladder's fan-out, instruments.cpp:238-266).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "device_types.hpp"
+#include "hjmsv_b200.h"
+#include "host_math.hpp"
+#include "lowering.hpp"
+
+using namespace hjmsv_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Failure : std::runtime_error {
+    int code;
+    Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Failure(HJMSV_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class F>
+int32_t guarded(F&& f) {
+    try {
+        f();
+        return HJMSV_OK;
+    } catch (const Failure& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return HJMSV_INVALID_ARGUMENT;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return HJMSV_DOMAIN;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return HJMSV_LOGIC;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return HJMSV_INVALID_ARGUMENT;
+    }
+}
+
+template <class T>
+T* dalloc(size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+void dfree(void* p) {
+    if (p) cudaFree(p);
+}
+
+}  // namespace
+
+struct hjmsv_solver {
+    int device = 0;
+    int mode = HJMSV_MODE_STRICT;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int P = 0, nr = 0, nv = 0, ny = 0, S = 0;
+    long long N = 0;
+    std::vector<double> maturity, spot_w_host;
+    std::vector<long long> spot_idx_host;
+    std::vector<std::vector<double>> term_steps;  // per problem: t_next per step
+    std::vector<double> bound;
+    // device
+    double *U = nullptr, *D = nullptr, *C = nullptr, *U0 = nullptr;
+    double *axes = nullptr, *steps = nullptr, *fast = nullptr;
+    ProblemConst* pc = nullptr;
+    DevStatus* st = nullptr;
+    long long* spot_idx = nullptr;
+    double *spot_w = nullptr, *spot_out = nullptr;
+    BatchView view{};
+    int step = 0;
+    double last_ms = 0.0;
+    long long last_launches = 0;
+    double wall_seconds = 0.0;
+    cudaGraphExec_t graph = nullptr;
+    long long graph_launches = 0;
+    std::vector<hjmsv_report> reports;
+    std::vector<std::string> messages;
+    std::vector<Lowered> low;  // host tables (init freed) for readouts
+    bool stage = false;        // single-step stage handle: messages unprefixed
+
+    ~hjmsv_solver() {
+        if (device >= 0) cudaSetDevice(device);
+        if (graph) cudaGraphExecDestroy(graph);
+        for (void* p : {(void*)U, (void*)D, (void*)C, (void*)U0, (void*)axes, (void*)steps,
+                        (void*)fast, (void*)pc, (void*)st, (void*)spot_idx, (void*)spot_w,
+                        (void*)spot_out})
+            dfree(p);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+void enqueue_steps(hjmsv_solver* h, int from, int count, long long* launches) {
+    for (int s = from; s < from + count; ++s) {
+        if (h->mode == HJMSV_MODE_FAST)
+            fast_step(h->view, s, h->stream, launches);
+        else
+            strict_step(h->view, s, h->stream, launches);
+    }
+}
+
+std::string status_message(hjmsv_solver* h, int p, const DevStatus& ds, int* code,
+                           int* row) {
+    const std::string prefix =
+        h->stage ? std::string()
+                 : "step " + std::to_string(ds.fail_step) + "/" + std::to_string(h->S) + ": ";
+    *row = -1;
+    if (ds.fail_code == HJMSV_SINGULAR_PIVOT) {
+        *code = HJMSV_SINGULAR_PIVOT;
+        *row = static_cast<int>(ds.pivot_key & 0xFFFFFull);
+        return prefix + "thomas_solve: singular pivot at row " + std::to_string(*row);
+    }
+    if (ds.nonfinite_first < ds.diverge_first) {
+        *code = HJMSV_NONFINITE;
+        return prefix + "solution left the finite range (NaN/Inf)";
+    }
+    *code = HJMSV_DIVERGED;
+    return prefix + "solution exceeded the divergence bound " + std::to_string(h->bound[p]);
+}
+
+int collect(hjmsv_solver* h) {
+    CK(cudaStreamSynchronize(h->stream));
+    std::vector<DevStatus> ds(h->P);
+    CK(cudaMemcpy(ds.data(), h->st, sizeof(DevStatus) * h->P, cudaMemcpyDeviceToHost));
+    int first = HJMSV_OK;
+    for (int p = 0; p < h->P; ++p) {
+        hjmsv_report& r = h->reports[p];
+        r.n_steps = h->S;
+        r.wall_seconds = h->wall_seconds;
+        if (ds[p].fail_step) {
+            int code = 0, row = -1;
+            h->messages[p] = status_message(h, p, ds[p], &code, &row);
+            r.status = code;
+            r.failed_step = ds[p].fail_step;
+            r.failed_row = row;
+            r.nan_guard_ok = 0;
+            r.steps_done = ds[p].fail_step - 1;
+            if (first == HJMSV_OK) {
+                first = code;
+                g_err = h->messages[p];
+            }
+        } else {
+            r.status = HJMSV_OK;
+            r.failed_step = 0;
+            r.failed_row = -1;
+            r.nan_guard_ok = 1;
+            r.steps_done = h->step;
+            double md;
+            const unsigned long long bits = ds[p].maxdelta_bits;
+            std::memcpy(&md, &bits, sizeof(md));
+            if (h->step > 0) r.last_max_delta = md;
+            // run() lands exactly on t = 0 after the march (solver.cpp:253)
+            r.time = h->step >= h->S ? 0.0
+                     : h->step == 0  ? h->maturity[p]
+                                     : h->term_steps[p][h->step - 1];
+        }
+    }
+    return first;
+}
+
+struct StageOverride {
+    double t_from = 0.0, dt = 0.0, dt_mult = 0.0;
+    bool faces = true, apply_only = false;
+};
+
+hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
+                            const hjmsv_solver_config& cfg, int device, int mode,
+                            const StageOverride* ov = nullptr) {
+    if (!problems || count < 1) throw std::invalid_argument("no problems given");
+    if (mode != HJMSV_MODE_STRICT && mode != HJMSV_MODE_FAST)
+        throw std::invalid_argument("unknown arithmetic mode");
+    std::vector<Lowered> L(count);
+    for (int p = 0; p < count; ++p) {
+        L[p] = lower_problem(problems[p], cfg, true);
+        if (ov) {  // one explicit level (t_from, dt): the douglas_step / apply_operator stages
+            L[p].n_steps = 1;
+            L[p].dt = ov->dt;
+            L[p].pc.dt = ov->dt_mult;
+            L[p].pc.theta_dt = cfg.theta_cn * ov->dt;
+            build_step_table(L[p], {ov->t_from}, ov->dt, ov->faces);
+        }
+        if (L[p].nr != L[0].nr || L[p].nv != L[0].nv || L[p].ny != L[0].ny ||
+            L[p].n_steps != L[0].n_steps)
+            throw std::invalid_argument("batched problems must share grid dims and step count");
+    }
+    if (mode == HJMSV_MODE_FAST && !fast_supported(L[0].nr, L[0].nv, L[0].ny))
+        throw Failure(HJMSV_UNSUPPORTED, "FAST kernels do not support this grid shape");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw std::invalid_argument("no such CUDA device");
+    auto h = std::make_unique<hjmsv_solver>();
+    h->device = device;
+    CK(cudaSetDevice(device));
+    h->mode = mode;
+    h->P = count;
+    h->nr = L[0].nr;
+    h->nv = L[0].nv;
+    h->ny = L[0].ny;
+    h->S = L[0].n_steps;
+    h->N = static_cast<long long>(h->nr) * h->nv * h->ny;
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&h->ev0));
+    CK(cudaEventCreate(&h->ev1));
+    const size_t PN = static_cast<size_t>(count) * h->N;
+    const int astride = axes_stride(h->nr, h->nv, h->ny);
+    h->U = dalloc<double>(PN);
+    h->D = dalloc<double>(PN);
+    h->U0 = dalloc<double>(PN);
+    if (mode == HJMSV_MODE_STRICT) h->C = dalloc<double>(PN);
+    h->axes = dalloc<double>(static_cast<size_t>(count) * astride);
+    h->steps = dalloc<double>(static_cast<size_t>(count) * h->S * kStepStride);
+    h->pc = dalloc<ProblemConst>(count);
+    h->st = dalloc<DevStatus>(count);
+    h->spot_idx = dalloc<long long>(static_cast<size_t>(count) * 8);
+    h->spot_w = dalloc<double>(static_cast<size_t>(count) * 8);
+    h->spot_out = dalloc<double>(count);
+    std::vector<ProblemConst> pcs(count);
+    h->spot_idx_host.resize(static_cast<size_t>(count) * 8);
+    h->spot_w_host.resize(static_cast<size_t>(count) * 8);
+    h->term_steps.resize(count);
+    for (int p = 0; p < count; ++p) {
+        const Lowered& l = L[p];
+        CK(cudaMemcpy(h->U0 + static_cast<size_t>(p) * h->N, l.init.data(),
+                      sizeof(double) * h->N, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->axes + static_cast<size_t>(p) * astride, l.axes.data(),
+                      sizeof(double) * astride, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->steps + static_cast<size_t>(p) * h->S * kStepStride, l.steps.data(),
+                      sizeof(double) * l.steps.size(), cudaMemcpyHostToDevice));
+        pcs[p] = l.pc;
+        std::copy(l.spot_idx, l.spot_idx + 8, h->spot_idx_host.begin() + p * 8);
+        std::copy(l.spot_w, l.spot_w + 8, h->spot_w_host.begin() + p * 8);
+        h->maturity.push_back(l.maturity);
+        h->bound.push_back(l.pc.bound);
+        for (int s = 0; s < h->S; ++s)
+            h->term_steps[p].push_back(l.steps[static_cast<size_t>(s) * kStepStride + ST_TNEXT]);
+    }
+    CK(cudaMemcpy(h->pc, pcs.data(), sizeof(ProblemConst) * count, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->spot_idx, h->spot_idx_host.data(), sizeof(long long) * 8 * count,
+                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->spot_w, h->spot_w_host.data(), sizeof(double) * 8 * count,
+                  cudaMemcpyHostToDevice));
+    BatchView& v = h->view;
+    v.P = count;
+    v.nr = h->nr;
+    v.nv = h->nv;
+    v.ny = h->ny;
+    v.N = h->N;
+    v.S = h->S;
+    v.y_order = cfg.y_boundary_order;
+    v.r_order = cfg.r_boundary_order;
+    v.dxr = L[0].r.dx();
+    v.dxv = L[0].v.dx();
+    v.dxy = L[0].y.dx();
+    v.U = h->U;
+    v.D = h->D;
+    v.C = h->C;
+    v.axes = h->axes;
+    v.axes_stride = astride;
+    v.pc = h->pc;
+    v.steps = h->steps;
+    v.st = h->st;
+    v.apply_only = ov && ov->apply_only ? 1 : 0;
+    h->stage = ov != nullptr;
+    if (mode == HJMSV_MODE_FAST) {
+        v.fast_stride = fast_stride(h->nr, h->nv, h->ny);
+        h->fast = dalloc<double>(static_cast<size_t>(count) * v.fast_stride);
+        v.fast = h->fast;
+        fast_prepare(v, h->stream);
+    }
+    h->reports.assign(count, hjmsv_report{});
+    h->messages.assign(count, std::string());
+    for (auto& r : h->reports) r.failed_row = -1;
+    CK(cudaMemcpyAsync(h->U, h->U0, sizeof(double) * PN, cudaMemcpyDeviceToDevice, h->stream));
+    reset_status(v, h->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    for (auto& l : L) {
+        l.init.clear();
+        l.init.shrink_to_fit();
+        l.steps.clear();
+        l.steps.shrink_to_fit();
+    }
+    h->low = std::move(L);
+    return h.release();
+}
+
+}  // namespace
+
+extern "C" {
+
+void hjmsv_default_solver_config(hjmsv_solver_config* cfg) {
+    if (cfg) *cfg = default_config();
+}
+
+const char* hjmsv_last_error(void) { return g_err.c_str(); }
+int32_t hjmsv_abi_version(void) { return HJMSV_ABI_VERSION; }
+
+int32_t hjmsv_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int32_t hjmsv_uniform_axis(double z0, double z_inf, int32_t n, double* z, double* j1, double* j2) {
+    return guarded([&] {
+        Axis a = make_uniform_axis(z0, z_inf, n);
+        std::copy(a.z.begin(), a.z.end(), z);
+        std::copy(a.j1.begin(), a.j1.end(), j1);
+        std::copy(a.j2.begin(), a.j2.end(), j2);
+    });
+}
+
+int32_t hjmsv_sinh_axis(double center, double alpha, double z0, double z_inf, int32_t n,
+                        double* z, double* j1, double* j2, double* c1c2) {
+    return guarded([&] {
+        Axis a = make_sinh_axis(center, alpha, z0, z_inf, n);
+        std::copy(a.z.begin(), a.z.end(), z);
+        std::copy(a.j1.begin(), a.j1.end(), j1);
+        std::copy(a.j2.begin(), a.j2.end(), j2);
+        if (c1c2) {
+            c1c2[0] = a.c1;
+            c1c2[1] = a.c2;
+        }
+    });
+}
+
+int32_t hjmsv_curve_eval(const hjmsv_curve* c, int32_t what, int32_t count, const double* t,
+                         double* out) {
+    return guarded([&] {
+        if (!c) throw std::invalid_argument("curve must be given");
+        hjmsv_problem tmp{};
+        Curve curve = c->kind == HJMSV_CURVE_FLAT
+                          ? Curve::flat(c->flat_base)
+                          : [&] {
+                                std::vector<std::pair<double, double>> nodes;
+                                for (int i = 0; i < c->n_nodes; ++i)
+                                    nodes.emplace_back(c->maturities[i], c->discounts[i]);
+                                return Curve::from_nodes(std::move(nodes));
+                            }();
+        (void)tmp;
+        for (int q = 0; q < count; ++q)
+            out[q] = what == 0   ? curve.discount(t[q])
+                     : what == 1 ? curve.forward(t[q])
+                                 : curve.forward_slope(t[q]);
+    });
+}
+
+int32_t hjmsv_zcb_closed_form(const hjmsv_curve* c, double kappa, double t, double maturity,
+                              double x, double y, double* out) {
+    return guarded([&] {
+        Curve curve = c->kind == HJMSV_CURVE_FLAT
+                          ? Curve::flat(c->flat_base)
+                          : [&] {
+                                std::vector<std::pair<double, double>> nodes;
+                                for (int i = 0; i < c->n_nodes; ++i)
+                                    nodes.emplace_back(c->maturities[i], c->discounts[i]);
+                                return Curve::from_nodes(std::move(nodes));
+                            }();
+        *out = zcb_closed_form(t, maturity, x, y, curve, kappa);
+    });
+}
+
+int32_t hjmsv_solver_create(const hjmsv_problem* problems, int32_t count,
+                            const hjmsv_solver_config* cfg, int32_t device, int32_t mode,
+                            hjmsv_solver** out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("output handle pointer is null");
+        *out = nullptr;
+        *out = create_handle(problems, count, cfg ? *cfg : default_config(), device, mode);
+    });
+}
+
+void hjmsv_solver_destroy(hjmsv_solver* h) { delete h; }
+
+int32_t hjmsv_solver_reset(hjmsv_solver* h) {
+    return guarded([&] {
+        if (!h) throw std::invalid_argument("null handle");
+        CK(cudaSetDevice(h->device));
+        CK(cudaMemcpyAsync(h->U, h->U0, sizeof(double) * h->P * h->N, cudaMemcpyDeviceToDevice,
+                           h->stream));
+        reset_status(h->view, h->stream);
+        CK(cudaGetLastError());
+        h->step = 0;
+        for (auto& r : h->reports) {
+            r = hjmsv_report{};
+            r.failed_row = -1;
+        }
+    });
+}
+
+int32_t hjmsv_solver_step_async(hjmsv_solver* h, int32_t steps) {
+    return guarded([&] {
+        if (!h) throw std::invalid_argument("null handle");
+        if (steps < 0) throw std::invalid_argument("step count must be nonnegative");
+        CK(cudaSetDevice(h->device));
+        const int count = std::min(steps, h->S - h->step);
+        h->last_launches = 0;
+        CK(cudaEventRecord(h->ev0, h->stream));
+        if (count > 0 && h->step == 0 && count == h->S) {
+            // the full march: one captured graph, instantiated once per handle
+            if (!h->graph) {
+                cudaGraph_t g = nullptr;
+                CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+                long long n = 0;
+                enqueue_steps(h, 0, h->S, &n);
+                CK(cudaStreamEndCapture(h->stream, &g));
+                CK(cudaGraphInstantiate(&h->graph, g, 0));
+                cudaGraphDestroy(g);
+                h->graph_launches = n;
+            }
+            CK(cudaGraphLaunch(h->graph, h->stream));
+            h->last_launches = h->graph_launches;
+        } else if (count > 0) {
+            enqueue_steps(h, h->step, count, &h->last_launches);
+        }
+        CK(cudaEventRecord(h->ev1, h->stream));
+        CK(cudaGetLastError());
+        h->step += count;
+    });
+}
+
+int32_t hjmsv_solver_synchronize(hjmsv_solver* h) {
+    int32_t first = HJMSV_OK;
+    int32_t code = guarded([&] {
+        if (!h) throw std::invalid_argument("null handle");
+        CK(cudaSetDevice(h->device));
+        first = collect(h);
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+        h->last_ms = ms;
+    });
+    return code != HJMSV_OK ? code : first;
+}
+
+int32_t hjmsv_solver_step(hjmsv_solver* h, int32_t steps) {
+    const auto t0 = std::chrono::steady_clock::now();
+    int32_t code = hjmsv_solver_step_async(h, steps);
+    if (code != HJMSV_OK) return code;
+    if (h) h->wall_seconds += 0.0;
+    code = hjmsv_solver_synchronize(h);
+    if (h) {
+        h->wall_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        for (auto& r : h->reports) r.wall_seconds = h->wall_seconds;
+    }
+    return code;
+}
+
+int32_t hjmsv_solver_run(hjmsv_solver* h) {
+    if (!h) {
+        g_err = "null handle";
+        return HJMSV_INVALID_ARGUMENT;
+    }
+    return hjmsv_solver_step(h, h->S - h->step);
+}
+
+int32_t hjmsv_solver_report(hjmsv_solver* h, int32_t problem, hjmsv_report* out) {
+    return guarded([&] {
+        if (!h || !out) throw std::invalid_argument("null argument");
+        if (problem < 0 || problem >= h->P) throw std::invalid_argument("problem index out of range");
+        *out = h->reports[problem];
+    });
+}
+
+int32_t hjmsv_solver_dims(hjmsv_solver* h, int32_t* nr, int32_t* nv, int32_t* ny,
+                          int32_t* count, int32_t* n_steps) {
+    return guarded([&] {
+        if (!h) throw std::invalid_argument("null handle");
+        if (nr) *nr = h->nr;
+        if (nv) *nv = h->nv;
+        if (ny) *ny = h->ny;
+        if (count) *count = h->P;
+        if (n_steps) *n_steps = h->S;
+    });
+}
+
+int32_t hjmsv_solver_get_grid(hjmsv_solver* h, int32_t problem, double* host_out) {
+    return guarded([&] {
+        if (!h || !host_out) throw std::invalid_argument("null argument");
+        if (problem < 0 || problem >= h->P) throw std::invalid_argument("problem index out of range");
+        CK(cudaSetDevice(h->device));
+        CK(cudaMemcpyAsync(host_out, h->U + static_cast<size_t>(problem) * h->N,
+                           sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int32_t hjmsv_solver_set_grid(hjmsv_solver* h, int32_t problem, const double* host_in,
+                              int32_t step_index) {
+    return guarded([&] {
+        if (!h || !host_in) throw std::invalid_argument("null argument");
+        if (problem < 0 || problem >= h->P) throw std::invalid_argument("problem index out of range");
+        if (step_index < 0 || step_index > h->S) throw std::invalid_argument("step index out of range");
+        CK(cudaSetDevice(h->device));
+        CK(cudaMemcpyAsync(h->U + static_cast<size_t>(problem) * h->N, host_in,
+                           sizeof(double) * h->N, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        h->step = step_index;
+    });
+}
+
+int32_t hjmsv_solver_price(hjmsv_solver* h, int32_t problem, double zr, double zv, double zy,
+                           double* out) {
+    return guarded([&] {
+        if (!h || !out) throw std::invalid_argument("null argument");
+        if (problem < 0 || problem >= h->P) throw std::invalid_argument("problem index out of range");
+        long long idx[8];
+        double w[8];
+        locate_point(h->low[problem], zr, zv, zy, idx, w);
+        CK(cudaSetDevice(h->device));
+        double val[8];
+        const double* U = h->U + static_cast<size_t>(problem) * h->N;
+        for (int c = 0; c < 8; ++c)
+            CK(cudaMemcpyAsync(&val[c], U + idx[c], sizeof(double), cudaMemcpyDeviceToHost,
+                               h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        double acc = 0.0;  // interpolate_at accumulation order (instruments.cpp:77-87)
+        for (int c = 0; c < 8; ++c) {
+            if (w[c] == 0.0) continue;
+            acc += w[c] * val[c];
+        }
+        *out = acc;
+    });
+}
+
+int32_t hjmsv_solver_spot_prices(hjmsv_solver* h, double* out) {
+    return guarded([&] {
+        if (!h || !out) throw std::invalid_argument("null argument");
+        CK(cudaSetDevice(h->device));
+        gather_spot(h->view, h->spot_idx, h->spot_w, h->spot_out, h->stream);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, h->spot_out, sizeof(double) * h->P, cudaMemcpyDeviceToHost,
+                           h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int32_t hjmsv_solver_device_grid(hjmsv_solver* h, int32_t problem, double** dev_ptr) {
+    return guarded([&] {
+        if (!h || !dev_ptr) throw std::invalid_argument("null argument");
+        if (problem < 0 || problem >= h->P) throw std::invalid_argument("problem index out of range");
+        *dev_ptr = h->U + static_cast<size_t>(problem) * h->N;
+    });
+}
+
+int32_t hjmsv_solver_last_device_ms(hjmsv_solver* h, double* ms) {
+    return guarded([&] {
+        if (!h || !ms) throw std::invalid_argument("null argument");
+        *ms = h->last_ms;
+    });
+}
+
+int32_t hjmsv_solver_last_launches(hjmsv_solver* h, int64_t* launches) {
+    return guarded([&] {
+        if (!h || !launches) throw std::invalid_argument("null argument");
+        *launches = h->last_launches;
+    });
+}
+
+int32_t hjmsv_apply_operator(const hjmsv_problem* p, const hjmsv_solver_config* cfg, double t,
+                             const double* u, double* out, int32_t mode) {
+    return guarded([&] {
+        if (!p || !u || !out) throw std::invalid_argument("null argument");
+        hjmsv_problem q = *p;
+        q.initial_grid = u;
+        q.n_steps = 1;
+        StageOverride ov;
+        ov.t_from = t;  // dt = 0: t_mid = t exactly
+        ov.dt = 0.0;
+        ov.dt_mult = 1.0;
+        ov.faces = false;
+        ov.apply_only = true;
+        const hjmsv_solver_config c = cfg ? *cfg : default_config();
+        std::unique_ptr<hjmsv_solver> h(create_handle(&q, 1, c, 0, mode, &ov));
+        if (mode == HJMSV_MODE_FAST)
+            fast_explicit(h->view, 0, h->stream);
+        else
+            strict_explicit(h->view, 0, h->stream);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, h->D, sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int32_t hjmsv_douglas_step(const hjmsv_problem* p, const hjmsv_solver_config* cfg,
+                           const double* u_in, double t_from, double dt, double* u_out,
+                           double* max_delta, int32_t mode) {
+    int32_t status = HJMSV_OK;
+    int32_t code = guarded([&] {
+        if (!p || !u_in || !u_out) throw std::invalid_argument("null argument");
+        hjmsv_problem q = *p;
+        q.initial_grid = u_in;
+        q.n_steps = 1;
+        StageOverride ov;
+        ov.t_from = t_from;
+        ov.dt = dt;
+        ov.dt_mult = dt;
+        const hjmsv_solver_config c = cfg ? *cfg : default_config();
+        std::unique_ptr<hjmsv_solver> h(create_handle(&q, 1, c, 0, mode, &ov));
+        status = hjmsv_solver_step(h.get(), 1);
+        CK(cudaMemcpyAsync(u_out, h->U, sizeof(double) * h->N, cudaMemcpyDeviceToHost,
+                           h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (max_delta) *max_delta = h->reports[0].last_max_delta;
+        if (status != HJMSV_OK) throw Failure(status, h->messages[0]);
+    });
+    return code;
+}
+
+int32_t hjmsv_thomas_batch(int32_t n, int32_t count, const double* lower, const double* diag,
+                           const double* upper, const double* super2, double* rhs,
+                           int32_t mode) {
+    return guarded([&] {
+        if (n < 0 || count < 0) throw std::invalid_argument("negative size");
+        if (n == 0 || count == 0) return;
+        if (!lower || !diag || !upper || !super2 || !rhs) throw std::invalid_argument("null argument");
+        CK(cudaSetDevice(0));
+        const size_t m = static_cast<size_t>(n) * count;
+        double *dl = dalloc<double>(m), *dd = dalloc<double>(m), *du = dalloc<double>(m);
+        double *ds2 = dalloc<double>(count), *dr = dalloc<double>(m), *dsc = dalloc<double>(m);
+        int* dfail = dalloc<int>(count);
+        auto cleanup = [&] {
+            for (void* q : {(void*)dl, (void*)dd, (void*)du, (void*)ds2, (void*)dr, (void*)dsc,
+                            (void*)dfail})
+                dfree(q);
+        };
+        try {
+            CK(cudaMemcpy(dl, lower, m * 8, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dd, diag, m * 8, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(du, upper, m * 8, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(ds2, super2, static_cast<size_t>(count) * 8, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dr, rhs, m * 8, cudaMemcpyHostToDevice));
+            thomas_batch(n, count, dl, dd, du, ds2, dr, dsc, dfail, mode, nullptr);
+            CK(cudaGetLastError());
+            CK(cudaDeviceSynchronize());
+            std::vector<int> fail(count);
+            CK(cudaMemcpy(fail.data(), dfail, sizeof(int) * count, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(rhs, dr, m * 8, cudaMemcpyDeviceToHost));
+            cleanup();
+            for (int q = 0; q < count; ++q)
+                if (fail[q] >= 0)
+                    throw Failure(HJMSV_SINGULAR_PIVOT,
+                                  "thomas_solve: singular pivot at row " + std::to_string(fail[q]));
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+    });
+}
+
+int32_t hjmsv_batch_run(const hjmsv_problem* problems, int32_t count,
+                        const hjmsv_solver_config* cfg, const int32_t* devices,
+                        int32_t n_devices, int32_t mode, double* prices_out,
+                        hjmsv_report* reports_out, double* grids_out) {
+    return guarded([&] {
+        if (!problems || count < 1) throw std::invalid_argument("no problems given");
+        std::vector<int> devs;
+        if (devices && n_devices > 0)
+            devs.assign(devices, devices + n_devices);
+        else
+            devs.push_back(0);
+        const int G = static_cast<int>(std::min<size_t>(devs.size(), static_cast<size_t>(count)));
+        const hjmsv_solver_config c = cfg ? *cfg : default_config();
+        // contiguous shards of ceil(count/G) problems
+        const int per = (count + G - 1) / G;
+        std::vector<std::thread> pool;
+        std::vector<int> codes(G, HJMSV_OK);
+        std::vector<std::string> errs(G);
+        for (int g = 0; g < G; ++g) {
+            const int lo = g * per, hi = std::min(count, lo + per);
+            if (lo >= hi) continue;
+            pool.emplace_back([&, g, lo, hi] {
+                hjmsv_solver* h = nullptr;
+                int code = hjmsv_solver_create(problems + lo, hi - lo, &c, devs[g], mode, &h);
+                if (code == HJMSV_OK) code = hjmsv_solver_run(h);
+                if (h) {
+                    const int run_code = code;
+                    std::vector<double> pr(hi - lo);
+                    code = hjmsv_solver_spot_prices(h, pr.data());
+                    for (int q = lo; q < hi; ++q) {
+                        hjmsv_report r{};
+                        hjmsv_solver_report(h, q - lo, &r);
+                        if (prices_out)
+                            prices_out[q] = r.status == HJMSV_OK ? pr[q - lo] : std::nan("");
+                        if (reports_out) reports_out[q] = r;
+                        if (grids_out)
+                            hjmsv_solver_get_grid(h, q - lo,
+                                                  grids_out + static_cast<size_t>(q) * h->N);
+                    }
+                    if (run_code != HJMSV_OK) code = run_code;
+                    hjmsv_solver_destroy(h);
+                }
+                codes[g] = code;
+                errs[g] = g_err;
+            });
+        }
+        for (auto& t : pool) t.join();
+        for (int g = 0; g < G; ++g)
+            if (codes[g] != HJMSV_OK) throw Failure(codes[g], errs[g]);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// device_types.hpp — plain-data layout shared by the host lowering and the
+// sm_100a kernels. One BatchView describes P independent problems with equal
+// (nr, nv, ny) and step count, laid out problem-major in HBM; each problem's
+// level uses the reference index order idx(i,j,k) = (i*nv + j)*ny + k
+// (discretization.hpp:27-29): r outermost, y contiguous.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace hjmsv_b200 {
+
+// Per-step scalar table entry (doubles), one per (problem, step).
+// c4(t_mid) (discretization.cpp:47) and the closed-form face scalars at t_next
+// (ratio = p(0,T_x)/p(0,t_next), G = g_factor(T_x - t_next)), model.cpp:48-54.
+constexpr int kMaxTerms = 12;  // two closed-form terms per face
+constexpr int kStepStride = 32;
+enum StepSlot : int {
+    ST_C4 = 0,
+    ST_FNEXT = 1,   // f(0, t_next)
+    ST_TNEXT = 2,
+    ST_TMID = 3,
+    ST_RATIO = 4,   // [kMaxTerms]
+    ST_G = 16       // [kMaxTerms]
+};
+
+// Face order = reference Face enum (discretization.hpp:84).
+enum FaceId : int { F_RMIN = 0, F_RMAX, F_VMIN, F_VMAX, F_YMIN, F_YMAX };
+enum FaceRuleId : int { RULE_DIRICHLET = 0, RULE_DEGENERATE = 1, RULE_ONE_SIDED = 2 };
+enum FaceValueKind : int { VAL_ZERO = 0, VAL_ZCB = 1, VAL_ZCB_DIFF = 2 };
+
+struct ProblemConst {
+    double kappa, theta, half_eps2, r0, dt, theta_dt, bound;
+    double coef[kMaxTerms];   // term 2f: +coef*P(t,T), term 2f+1: -coef*P(t,T)
+    int rule[6];
+    int kind[6];
+};
+
+// Device status words per problem. A failing step sets fail_step (1-based);
+// every later kernel of that problem returns immediately, mirroring the
+// reference throwing out of douglas_step (solver.cpp:241-247).
+struct DevStatus {
+    int fail_step;
+    int fail_code;                          // hjmsv_status of the failure
+    unsigned long long pivot_key;           // (sweep<<50)|(line<<20)|row, first in loop order
+    unsigned long long nonfinite_first;     // first flat index with !isfinite (solver.cpp:71)
+    unsigned long long diverge_first;       // first flat index with |U| > bound (solver.cpp:73)
+    unsigned long long maxdelta_bits;       // max |dU| of the latest step (solver.cpp:163-167)
+};
+
+struct BatchView {
+    int P, nr, nv, ny;
+    long long N;          // nr*nv*ny
+    int S;                // steps in the march
+    int y_order, r_order;
+    double dxr, dxv, dxy;
+    double* U;            // [P][N] level
+    double* D;            // [P][N] delta / line workspace
+    double* C;            // [P][N] Thomas c' scratch (strict sweeps)
+    const double* axes;   // [P][axes_stride]: rz rj1 rj2 | vz vj1 vj2 | yz yj1 yj2 | a b
+    int axes_stride;
+    const ProblemConst* pc;
+    const double* steps;  // [P][S][kStepStride]
+    DevStatus* st;        // [P]
+    const double* fast;   // [P][fast_stride] derived factor tables (FAST mode)
+    int fast_stride;
+    int apply_only;       // stage mode: D = F(U), Dirichlet nodes 0 (apply_operator)
+};
+
+inline int axes_stride(int nr, int nv, int ny) { return 5 * nr + 3 * nv + 3 * ny; }
+
+// Kernel launch entry points (kernels_strict.cu / kernels_fast.cu).
+void strict_step(const BatchView& v, int s, cudaStream_t stream, long long* launches);
+void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launches);
+// explicit stage alone (stage test of apply_operator / dU0)
+void strict_explicit(const BatchView& v, int s, cudaStream_t stream);
+void fast_explicit(const BatchView& v, int s, cudaStream_t stream);
+void fast_prepare(const BatchView& v, cudaStream_t stream);  // builds v.fast from tables
+int fast_stride(int nr, int nv, int ny);
+bool fast_supported(int nr, int nv, int ny);
+void reset_status(const BatchView& v, cudaStream_t stream);
+// trilinear readout: out[p] = sum_q w[p*8+q] * U[p][idx[p*8+q]] (instruments.cpp:71-88)
+void gather_spot(const BatchView& v, const long long* idx, const double* w, double* out,
+                 cudaStream_t stream);
+// standalone batched Thomas (parity stage test of solver.cpp:22-57)
+void thomas_batch(int n, int count, const double* lower, const double* diag, const double* upper,
+                  const double* super2, double* rhs, double* scratch, int* fail_row, int fast,
+                  cudaStream_t stream);
+
+}  // namespace hjmsv_b200

@@ -1,0 +1,48 @@
+// lowering.hpp — PdeProblem + SolverConfig (as hjmsv_problem / hjmsv_solver_config)
+// lowered on the host to the plain tables the device kernels read.
+#pragma once
+
+#include <vector>
+
+#include "device_types.hpp"
+#include "hjmsv_b200.h"
+#include "host_math.hpp"
+
+namespace hjmsv_b200 {
+
+struct Lowered {
+    int nr = 0, nv = 0, ny = 0;
+    int n_steps = 0;
+    double maturity = 0.0, dt = 0.0, r0 = 0.0;
+    Axis r, v, y;
+    Curve curve;
+    ProblemConst pc{};
+    std::vector<double> axes;    // axes_stride(nr,nv,ny)
+    std::vector<double> steps;   // n_steps * kStepStride
+    std::vector<double> init;    // nr*nv*ny level at t = T
+    double term_t[kMaxTerms] = {};  // maturity of each closed-form term slot
+    long long spot_idx[8] = {};  // interpolate_at corners at natural_spot
+    double spot_w[8] = {};
+};
+
+/// Validates exactly like run() (solver.cpp:214-216), SolverConfig::validate
+/// (solver.cpp:10-20), ModelParams::validate (model.cpp:25-33), CapletSpec::validate
+/// (model.cpp:35-39), HjmCoefficientField (discretization.cpp:34-35) and
+/// SpatialOperator (discretization.cpp:144-150), then builds every table.
+/// Throws the reference's exception types/messages.
+Lowered lower_problem(const hjmsv_problem& p, const hjmsv_solver_config& cfg, bool build_init);
+
+/// Per-step scalar table for explicit (t_from, dt) levels; used by the march
+/// (time levels of run() or the indexed harness) and by the single-step stage.
+void build_step_table(Lowered& L, const std::vector<double>& t_from, double dt, bool faces);
+
+/// Time levels t_from[s] of the march (solver.cpp:85-87 or SURVEY §8c).
+std::vector<double> march_levels(double maturity, int n_steps, int time_levels);
+
+/// Corner indices/weights of interpolate_at (instruments.cpp:71-88) at (zr, zv, zy).
+void locate_point(const Lowered& L, double zr, double zv, double zy, long long idx[8],
+                  double w[8]);
+
+hjmsv_solver_config default_config();
+
+}  // namespace hjmsv_b200
