@@ -219,6 +219,14 @@ int32_t hjmsv_solver_last_device_ms(hjmsv_solver* h, double* ms);
 /* Number of kernel launches issued by the last step_async call. */
 int32_t hjmsv_solver_last_launches(hjmsv_solver* h, int64_t* launches);
 
+/* Live per-kernel profile: runs `steps` steps with a CUDA event after every
+ * launch; returns each kernel's average duration (ms), its ALGORITHMIC bytes
+ * per launch (bytes/point x points; SURVEY §8d accounting), the launch count,
+ * and names (name_len bytes each). Used by bench.py for the roofline. */
+int32_t hjmsv_solver_kernel_profile(hjmsv_solver* h, int32_t steps, int32_t max_kernels,
+                                    double* avg_ms, double* alg_bytes, int64_t* launches,
+                                    int32_t* n_kernels, char* names, int32_t name_len);
+
 /* ---- stage entry points (parity tests: the reference's stage oracles) ---- */
 /* SpatialOperator::apply_operator after coefficients().prepare(t) (discretization.cpp:302-364) */
 int32_t hjmsv_apply_operator(const hjmsv_problem* p, const hjmsv_solver_config* cfg, double t,

@@ -98,6 +98,8 @@ SIGNATURES = {
     "hjmsv_solver_device_grid": (I32, [HP, I32, POINTER(PD)]),
     "hjmsv_solver_last_device_ms": (I32, [HP, PD]),
     "hjmsv_solver_last_launches": (I32, [HP, POINTER(c_int64)]),
+    "hjmsv_solver_kernel_profile": (I32, [HP, I32, I32, PD, PD, POINTER(c_int64), POINTER(I32),
+                                          ctypes.c_char_p, I32]),
     "hjmsv_apply_operator": (I32, [POINTER(CProblem), POINTER(CSolverConfig), c_double, PD, PD, I32]),
     "hjmsv_douglas_step": (I32, [POINTER(CProblem), POINTER(CSolverConfig), PD, c_double, c_double, PD, PD, I32]),
     "hjmsv_thomas_batch": (I32, [I32, I32, PD, PD, PD, PD, PD, I32]),

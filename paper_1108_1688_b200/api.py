@@ -170,6 +170,20 @@ class Solver:
         _check(self.lib.hjmsv_solver_last_device_ms(self.h, ctypes.byref(ms)))
         return ms.value
 
+    def kernel_profile(self, steps: int):
+        """Per-kernel average ms and algorithmic bytes per launch over `steps` steps."""
+        K, L = 16, 64
+        ms, by = np.zeros(K), np.zeros(K)
+        n, nk = ctypes.c_int64(), ctypes.c_int32()
+        names = ctypes.create_string_buffer(K * L)
+        _check(self.lib.hjmsv_solver_kernel_profile(self.h, steps, K, _ptr(ms), _ptr(by),
+                                                    ctypes.byref(n), ctypes.byref(nk), names, L))
+        out = []
+        for q in range(nk.value):
+            nm = names.raw[q * L:(q + 1) * L].split(b"\0", 1)[0].decode()
+            out.append({"name": nm, "avg_ms": float(ms[q]), "alg_bytes": float(by[q])})
+        return out, n.value
+
     def last_launches(self) -> int:
         n = ctypes.c_int64()
         _check(self.lib.hjmsv_solver_last_launches(self.h, ctypes.byref(n)))

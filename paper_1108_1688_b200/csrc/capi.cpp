@@ -41,6 +41,13 @@ template <class F>
 int32_t guarded(F&& f) {
     try {
         f();
+        // surface any asynchronous/unchecked CUDA error at the call that caused it
+        const cudaError_t pending = cudaGetLastError();
+        if (pending != cudaSuccess && pending != cudaErrorNoDevice &&
+            pending != cudaErrorInsufficientDriver) {
+            g_err = std::string("CUDA error pending after call: ") + cudaGetErrorString(pending);
+            return HJMSV_CUDA_ERROR;
+        }
         return HJMSV_OK;
     } catch (const Failure& e) {
         g_err = e.what();
@@ -234,7 +241,7 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
     h->U = dalloc<double>(PN);
     h->D = dalloc<double>(PN);
     h->U0 = dalloc<double>(PN);
-    if (mode == HJMSV_MODE_STRICT) h->C = dalloc<double>(PN);
+    h->C = dalloc<double>(PN);
     h->axes = dalloc<double>(static_cast<size_t>(count) * astride);
     h->steps = dalloc<double>(static_cast<size_t>(count) * h->S * kStepStride);
     h->pc = dalloc<ProblemConst>(count);
@@ -293,6 +300,11 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         v.fast_stride = fast_stride(h->nr, h->nv, h->ny);
         h->fast = dalloc<double>(static_cast<size_t>(count) * v.fast_stride);
         v.fast = h->fast;
+        for (int p = 0; p < count; ++p) {
+            const std::vector<double> ft = build_fast_tables(L[p], cfg, L[p].pc.theta_dt);
+            CK(cudaMemcpy(h->fast + static_cast<size_t>(p) * v.fast_stride, ft.data(),
+                          sizeof(double) * ft.size(), cudaMemcpyHostToDevice));
+        }
         fast_prepare(v, h->stream);
     }
     h->reports.assign(count, hjmsv_report{});
@@ -312,9 +324,93 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
     return h.release();
 }
 
+struct ProfCtx {
+    cudaStream_t stream;
+    std::vector<cudaEvent_t>* events;
+    std::vector<std::string>* names;
+    std::vector<double>* bytes;
+    std::vector<int>* idx;
+};
+
+void prof_after(void* vctx, int idx, const char* name, double b) {
+    auto* c = static_cast<ProfCtx*>(vctx);
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c->stream);
+    c->events->push_back(e);
+    c->names->push_back(name);
+    c->bytes->push_back(b);
+    c->idx->push_back(idx);
+}
+
 }  // namespace
 
 extern "C" {
+
+int32_t hjmsv_solver_kernel_profile(hjmsv_solver* h, int32_t steps, int32_t max_kernels,
+                                    double* avg_ms, double* alg_bytes, int64_t* launches_out,
+                                    int32_t* n_kernels, char* names, int32_t name_len) {
+    return guarded([&] {
+        if (!h || !avg_ms || !alg_bytes || !n_kernels) throw std::invalid_argument("null argument");
+        CK(cudaSetDevice(h->device));
+        const int count = std::min(steps, h->S - h->step);
+        std::vector<cudaEvent_t> ev;
+        std::vector<std::string> nm;
+        std::vector<double> by;
+        std::vector<int> ix;
+        ProfCtx ctx{h->stream, &ev, &nm, &by, &ix};
+        LaunchHook hook;
+        hook.after = prof_after;
+        hook.ctx = &ctx;
+        cudaEvent_t start;
+        CK(cudaEventCreate(&start));
+        CK(cudaEventRecord(start, h->stream));
+        long long n = 0;
+        for (int s = h->step; s < h->step + count; ++s) {
+            if (h->mode == HJMSV_MODE_FAST)
+                fast_step(h->view, s, h->stream, &n, &hook);
+            else
+                strict_step(h->view, s, h->stream, &n, &hook);
+        }
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->stream));
+        h->step += count;
+        std::vector<double> total;
+        std::vector<int> calls;
+        std::vector<std::string> kn;
+        std::vector<double> kb;
+        cudaEvent_t prev = start;
+        for (size_t q = 0; q < ev.size(); ++q) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, prev, ev[q]));
+            prev = ev[q];
+            const int id = ix[q];
+            if (id >= static_cast<int>(total.size())) {
+                total.resize(id + 1, 0.0);
+                calls.resize(id + 1, 0);
+                kn.resize(id + 1);
+                kb.resize(id + 1, 0.0);
+            }
+            total[id] += ms;
+            calls[id] += 1;
+            kn[id] = nm[q];
+            kb[id] = by[q] * static_cast<double>(h->N) * h->P;
+        }
+        for (auto e : ev) cudaEventDestroy(e);
+        cudaEventDestroy(start);
+        const int K = std::min<int>(max_kernels, static_cast<int>(total.size()));
+        for (int q = 0; q < K; ++q) {
+            avg_ms[q] = calls[q] ? total[q] / calls[q] : 0.0;
+            alg_bytes[q] = kb[q];
+            if (names && name_len > 0) {
+                std::strncpy(names + static_cast<size_t>(q) * name_len, kn[q].c_str(), name_len - 1);
+                names[static_cast<size_t>(q) * name_len + name_len - 1] = 0;
+            }
+        }
+        *n_kernels = K;
+        if (launches_out) *launches_out = n;
+    });
+}
 
 void hjmsv_default_solver_config(hjmsv_solver_config* cfg) {
     if (cfg) *cfg = default_config();

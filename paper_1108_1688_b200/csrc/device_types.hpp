@@ -70,9 +70,31 @@ struct BatchView {
 
 inline int axes_stride(int nr, int nv, int ny) { return 5 * nr + 3 * nv + 3 * ny; }
 
+// FAST-mode factor tables per problem (host-built, lowering.cpp): the
+// separable pieces of g1..g6 (discretization.cpp:56-72) with the stencil
+// 1/dx factors folded in, plus the v-line LU, which depends on j only.
+//   g1/dxr^2      = G1[i]*v_j            g4/(2dxr) = c4*G4C[i] + G4P[i] + G4Q[i]*y_k + G4V[i]*v_j
+//   g3/(4dxr dxv) = G3[i]*G3V[j]         g2/dxv^2  = G2[j],  g5/(2dxv) = G5[j]
+//   g6/(2dxy)     = a_i v_j S6[k] + T6[k]           reaction = REACT[i]
+enum FastR : int { FR_G1 = 0, FR_G4C, FR_G4P, FR_G4Q, FR_G4V, FR_G3, FR_REACT, FR_A, FR_COUNT };
+enum FastV : int { FV_V = 0, FV_G2, FV_G5, FV_G3, FV_L, FV_CP, FV_RP, FV_COUNT };
+enum FastY : int { FY_S6 = 0, FY_T6, FY_COUNT };
+inline int fast_table_stride(int nr, int nv, int ny) {
+    return FR_COUNT * nr + FV_COUNT * nv + FY_COUNT * ny;
+}
+
+// Per-kernel hook for the live profiler: called after each launch with the
+// kernel's index, name and ALGORITHMIC bytes per grid point of that launch.
+struct LaunchHook {
+    void (*after)(void* ctx, int idx, const char* name, double alg_bytes_per_point) = nullptr;
+    void* ctx = nullptr;
+};
+
 // Kernel launch entry points (kernels_strict.cu / kernels_fast.cu).
-void strict_step(const BatchView& v, int s, cudaStream_t stream, long long* launches);
-void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launches);
+void strict_step(const BatchView& v, int s, cudaStream_t stream, long long* launches,
+                 const LaunchHook* hook = nullptr);
+void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launches,
+               const LaunchHook* hook = nullptr);
 // explicit stage alone (stage test of apply_operator / dU0)
 void strict_explicit(const BatchView& v, int s, cudaStream_t stream);
 void fast_explicit(const BatchView& v, int s, cudaStream_t stream);

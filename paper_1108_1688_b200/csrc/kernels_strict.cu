@@ -16,87 +16,11 @@
 #include <cfloat>
 #include <cmath>
 
-#include "device_types.hpp"
-#include "hjmsv_b200.h"
+#include "kernels_common.cuh"
 
 namespace hjmsv_b200 {
 namespace {
-
-struct Tab {
-    const double *rz, *rj1, *rj2, *vz, *vj1, *vj2, *yz, *yj1, *yj2, *a, *b;
-};
-
-__device__ __forceinline__ Tab tables(const BatchView& v, int p) {
-    const double* t = v.axes + static_cast<size_t>(p) * v.axes_stride;
-    Tab x;
-    x.rz = t;
-    x.rj1 = t + v.nr;
-    x.rj2 = t + 2 * v.nr;
-    t += 3 * v.nr;
-    x.vz = t;
-    x.vj1 = t + v.nv;
-    x.vj2 = t + 2 * v.nv;
-    t += 3 * v.nv;
-    x.yz = t;
-    x.yj1 = t + v.ny;
-    x.yj2 = t + 2 * v.ny;
-    t += 3 * v.ny;
-    x.a = t;
-    x.b = t + v.nr;
-    return x;
-}
-
-// SpatialOperator::is_dirichlet (discretization.cpp:153-170)
-__device__ __forceinline__ bool is_dirichlet(const BatchView& v, const ProblemConst& pc, int i,
-                                             int j, int k) {
-    if (v.nr > 1) {
-        if (i == 0 && pc.rule[F_RMIN] == RULE_DIRICHLET) return true;
-        if (i == v.nr - 1 && pc.rule[F_RMAX] == RULE_DIRICHLET) return true;
-    }
-    if (v.nv > 1) {
-        if (j == 0 && pc.rule[F_VMIN] == RULE_DIRICHLET) return true;
-        if (j == v.nv - 1 && pc.rule[F_VMAX] == RULE_DIRICHLET) return true;
-    }
-    if (v.ny > 1) {
-        if (k == 0 && pc.rule[F_YMIN] == RULE_DIRICHLET) return true;
-        if (k == v.ny - 1 && pc.rule[F_YMAX] == RULE_DIRICHLET) return true;
-    }
-    return false;
-}
-
-// dirichlet_value precedence r_max > y_max > v_max > r_min > y_min > v_min
-// (discretization.cpp:172-192); -1 when the node is not Dirichlet.
-__device__ __forceinline__ int dirichlet_face(const BatchView& v, const ProblemConst& pc, int i,
-                                              int j, int k) {
-    auto act = [&](int f, bool on) { return on && pc.rule[f] == RULE_DIRICHLET; };
-    if (act(F_RMAX, v.nr > 1 && i == v.nr - 1)) return F_RMAX;
-    if (act(F_YMAX, v.ny > 1 && k == v.ny - 1)) return F_YMAX;
-    if (act(F_VMAX, v.nv > 1 && j == v.nv - 1)) return F_VMAX;
-    if (act(F_RMIN, v.nr > 1 && i == 0)) return F_RMIN;
-    if (act(F_YMIN, v.ny > 1 && k == 0)) return F_YMIN;
-    if (act(F_VMIN, v.nv > 1 && j == 0)) return F_VMIN;
-    return -1;
-}
-
-// closed-form face value: coef*P(t,T1) [- coef'*P(t,T2)], P = ratio*exp(-G x - G^2 y/2)
-// with x = r0*zr - f(0,t), y = r0^2*zy (discretization.cpp:77-81,111-118; model.cpp:48-54)
-__device__ __forceinline__ double face_value(const ProblemConst& pc, const double* step,
-                                             const Tab& T, int face, int i, int k) {
-    const int kind = pc.kind[face];
-    if (kind == VAL_ZERO) return 0.0;
-    const double x = pc.r0 * T.rz[i] - step[ST_FNEXT];
-    const double y = pc.r0 * pc.r0 * T.yz[k];
-    const int t0 = 2 * face;
-    const double g1 = step[ST_G + t0];
-    const double p1 = step[ST_RATIO + t0] * exp(-g1 * x - 0.5 * g1 * g1 * y);
-    double val = pc.coef[t0] * p1;
-    if (kind == VAL_ZCB_DIFF) {
-        const double g2 = step[ST_G + t0 + 1];
-        const double p2 = step[ST_RATIO + t0 + 1] * exp(-g2 * x - 0.5 * g2 * g2 * y);
-        val = val - pc.coef[t0 + 1] * p2;
-    }
-    return val;
-}
+using namespace dev;
 
 struct G {
     double g1, g2, g3, g4, g5, g6, reaction;
@@ -119,14 +43,6 @@ __device__ __forceinline__ G coeff(const ProblemConst& pc, const Tab& T, double 
     g.g6 = (2.0 * h1 - 2.0 * pc.kappa * yt) / T.yj1[k];
     g.reaction = T.rz[i] * pc.r0;
     return g;
-}
-
-__device__ __forceinline__ const double* step_row(const BatchView& v, int p, int s) {
-    return v.steps + (static_cast<size_t>(p) * v.S + s) * kStepStride;
-}
-
-__device__ __forceinline__ void mark_fail(DevStatus& st, int step1, int code) {
-    if (atomicCAS(&st.fail_step, 0, step1) == 0) st.fail_code = code;
 }
 
 // ---------------------------------------------------------------- explicit
@@ -447,24 +363,31 @@ __global__ void k_thomas_batch(int n, int count, const double* lower, const doub
 
 }  // namespace
 
-void strict_step(const BatchView& v, int s, cudaStream_t stream, long long* launches) {
+void strict_step(const BatchView& v, int s, cudaStream_t stream, long long* launches,
+                 const LaunchHook* hook) {
+    auto mark = [&](int idx, const char* name, double bytes) {
+        if (launches) ++*launches;
+        if (hook && hook->after) hook->after(hook->ctx, idx, name, bytes);
+    };
     const int tpb = 256;
     const dim3 grid_pts(static_cast<unsigned>((v.N + tpb - 1) / tpb), v.P);
+    // algorithmic bytes/point: read U, write dU (16) | read+write the line (16) |
+    // read dU, read U, write U (24)
     k_explicit<<<grid_pts, tpb, 0, stream>>>(v, s);
-    long long n = 1;
+    mark(0, "strict_explicit", 16.0);
     const int ltpb = 128;
     if (v.nr > 1) {
         k_sweep<AX_R><<<dim3((v.nv * v.ny + ltpb - 1) / ltpb, v.P), ltpb, 0, stream>>>(v, s);
-        ++n;
+        mark(1, "strict_sweep_r", 16.0);
     }
     if (v.nv > 1) {
         k_sweep<AX_V><<<dim3((v.nr * v.ny + ltpb - 1) / ltpb, v.P), ltpb, 0, stream>>>(v, s);
-        ++n;
+        mark(2, "strict_sweep_v", 16.0);
     }
     k_sweep<AX_Y><<<dim3((v.nr * v.nv + ltpb - 1) / ltpb, v.P), ltpb, 0, stream>>>(v, s);
+    mark(3, "strict_sweep_y", 16.0);
     k_update<<<grid_pts, tpb, 0, stream>>>(v, s);
-    n += 2;
-    if (launches) *launches += n;
+    mark(4, "strict_update", 24.0);
 }
 
 void strict_explicit(const BatchView& v, int s, cudaStream_t stream) {

@@ -45,4 +45,8 @@ void locate_point(const Lowered& L, double zr, double zv, double zy, long long i
 
 hjmsv_solver_config default_config();
 
+/// FAST-mode factor tables (layout: FastR/FastV/FastY in device_types.hpp).
+std::vector<double> build_fast_tables(const Lowered& L, const hjmsv_solver_config& cfg,
+                                      double theta_dt);
+
 }  // namespace hjmsv_b200

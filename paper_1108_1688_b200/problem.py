@@ -44,6 +44,7 @@ class AxisSpec:
     @staticmethod
     def uniform(z0: float, z_inf: float, n: int) -> "AxisSpec":
         """uniform_axis (mesh.cpp:46-62), same IEEE operations."""
+        z0, z_inf = float(z0), float(z_inf)
         if not z0 < z_inf:
             raise ValueError("axis requires z0 < z_inf")
         if n < 3:

@@ -1,0 +1,205 @@
+"""GPU parity: the sm_100a path through the C-ABI vs the oracle restatement.
+
+Bar (BASELINE north_star): |p_gpu - p_ref| <= 1e-10 |p_ref| and
+max|U_gpu - U_ref| <= 1e-10 max|U_ref|, per problem, FP64. STRICT mode keeps
+the reference's operation order, so it is held to a tighter 1e-13 on grids.
+"""
+import numpy as np
+import pytest
+
+import paper_1108_1688_b200 as hj
+from paper_1108_1688_b200 import workloads as W
+from paper_1108_1688_b200.problem import AxisSpec
+from oracle import bindings as B
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10          # north_star parity tolerance (relative, FP64)
+STRICT_TOL = 1e-13   # strict mode: reference operation order, only libm exp ulps differ
+MODES = ["strict", "fast"]
+
+
+def tol_for(mode):
+    return STRICT_TOL if mode == "strict" else TOL
+
+
+def solve(problems, mode, steps=None):
+    with hj.Solver(problems, mode=mode) as s:
+        if steps is None:
+            s.run()
+        else:
+            s.step(steps)
+        grids = [s.grid(q) for q in range(len(problems))]
+        prices = s.spot_prices()
+        reps = [s.report(q) for q in range(len(problems))]
+        launches = s.last_launches()
+    return grids, prices, reps, launches
+
+
+def assert_parity(p, g, price, oracle, mode, steps=-1):
+    g_ref, rep_ref, _, _ = oracle.run(p, steps=steps)
+    err = B.normwise_rel(g, g_ref)
+    assert err <= tol_for(mode), f"grid normwise rel err {err:.3e}"
+    if steps < 0:
+        p_ref = oracle.spot_price(p, g_ref)
+        perr = abs(price - p_ref) / abs(p_ref)
+        assert perr <= TOL, f"price rel err {perr:.3e} ({price} vs {p_ref})"
+    return g_ref, rep_ref
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_config0_full_march(gpu, oracle, mode):
+    p = W.make_problem(0, 0)
+    grids, prices, reps, launches = solve([p], mode)
+    _, rep_ref = assert_parity(p, grids[0], prices[0], oracle, mode)
+    assert reps[0]["status"] == 0 and reps[0]["steps_done"] == 200
+    assert abs(reps[0]["last_max_delta"] - rep_ref["last_max_delta"]) <= 1e-10 * rep_ref["last_max_delta"]
+    assert launches > 0
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_config2_reduced_caplet(gpu, oracle, mode):
+    p = W.make_problem(2, 3, nr=48, nv=24, ny=24, steps=60)
+    grids, prices, _, _ = solve([p], mode)
+    assert_parity(p, grids[0], prices[0], oracle, mode)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_config4_batch(gpu, oracle, mode):
+    probs = W.make_config(4, count=12)
+    kinds = {p.instrument for p in probs}
+    assert kinds == {0, 1}, "the batch must mix ZCBs and caplets"
+    grids, prices, reps, _ = solve(probs, mode)
+    for q, p in enumerate(probs):
+        assert reps[q]["status"] == 0
+        assert_parity(p, grids[q], prices[q], oracle, mode)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_sinh_mesh_caplet(gpu, oracle, mode):
+    """Non-uniform j1/j2: the reference's caplet_default metric (instruments.cpp:11-22)."""
+    p = W.make_problem(2, 1, nr=40, nv=20, ny=20, steps=30)
+    k_scaled = p.strike / p.r0
+    p.r = AxisSpec.sinh(k_scaled, 0.05, 0.0, 250.0, 40)
+    p.v = AxisSpec.sinh(0.5, 0.5, 0.0, 30.0, 20)
+    p.y = AxisSpec.sinh(0.0, 0.05, 0.0, 250.0, 20)
+    grids, prices, _, _ = solve([p], mode)
+    assert_parity(p, grids[0], prices[0], oracle, mode)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_config1_prefix_full_size(gpu, oracle, mode):
+    p = W.make_problem(1, 0)
+    grids, _, reps, _ = solve([p], mode, steps=4)
+    assert reps[0]["steps_done"] == 4
+    assert_parity(p, grids[0], None, oracle, mode, steps=4)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_config3_prefix_full_size(gpu, oracle, mode):
+    p = W.make_problem(3, 0)
+    grids, _, _, _ = solve([p], mode, steps=1)
+    assert_parity(p, grids[0], None, oracle, mode, steps=1)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_step_by_step_matches_full_march(gpu, mode):
+    p = W.make_problem(0, 1, nr=32, nv=16, ny=16, steps=30)
+    with hj.Solver([p], mode=mode) as s:
+        for _ in range(30):
+            s.step(1)
+        g1 = s.grid(0)
+        s.reset()
+        s.run()
+        g2 = s.grid(0)
+    assert np.array_equal(g1, g2)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_apply_operator_stage(gpu, oracle, mode):
+    p = W.make_problem(2, 2, nr=24, nv=12, ny=16, steps=10)
+    rng = np.random.default_rng(7)
+    u = oracle.initial_level(p) + 1e-3 * rng.standard_normal(p.shape)
+    for t in (p.maturity, 0.5 * p.maturity, 0.0):
+        f_ref = oracle.apply_operator(p, t, u)
+        f = hj.apply_operator(p, t, u, mode=mode)
+        assert B.normwise_rel(f, f_ref) <= tol_for(mode) * 10
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_douglas_step_stage(gpu, oracle, mode):
+    p = W.make_problem(4, 5, steps=200)
+    rng = np.random.default_rng(11)
+    u = oracle.initial_level(p) * (1 + 1e-4 * rng.standard_normal(p.shape))
+    dt = p.maturity / 200
+    ref, md_ref, code, _ = oracle.douglas_step(p, u, p.maturity, dt)
+    assert code == 0
+    out, md = hj.douglas_step(p, u, p.maturity, dt, mode=mode)
+    assert B.normwise_rel(out, ref) <= tol_for(mode)
+    assert abs(md - md_ref) <= 1e-10 * md_ref
+
+
+def test_thomas_batch_matches_reference_solver(gpu, oracle):
+    rng = np.random.default_rng(3)
+    count, n = 64, 50
+    lower = rng.uniform(-1, 1, (count, n))
+    upper = rng.uniform(-1, 1, (count, n))
+    diag = 3.0 + rng.uniform(0, 1, (count, n))
+    lower[:, 0] = 0.0
+    upper[:, -1] = 0.0
+    s2 = rng.uniform(-0.5, 0.5, count)
+    s2[::4] = 0.0
+    rhs = rng.standard_normal((count, n))
+    x_ref, code, _ = oracle.thomas(lower, diag, upper, s2, rhs)
+    assert code == 0
+    x = hj.thomas_batch(lower, diag, upper, s2, rhs, mode="strict")
+    assert np.array_equal(x, x_ref)
+
+
+def test_thomas_singular_pivot_message(gpu):
+    n = 5
+    lower, diag, upper = np.zeros((1, n)), np.ones((1, n)), np.zeros((1, n))
+    diag[0, 2] = 0.0
+    with pytest.raises(hj.SingularPivot, match="thomas_solve: singular pivot at row 2"):
+        hj.thomas_batch(lower, diag, upper, np.zeros(1), np.ones((1, n)))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_divergence_parity(gpu, oracle, mode):
+    """Wide variance domain v in [0,30] diverges; the GPU must flag it."""
+    p = W.make_problem(0, 0)
+    p.v = AxisSpec.uniform(0.0, 30.0, 32)
+    _, rep_ref, code_ref, msg_ref = oracle.run(p, raise_on_error=False)
+    assert code_ref == 4 and rep_ref["failed_step"] > 0
+    with hj.Solver([p], mode=mode) as s:
+        with pytest.raises(hj.Diverged) as ei:
+            s.run()
+        rep = s.report(0)
+    assert rep["status"] == 4
+    if mode == "strict":
+        assert rep["failed_step"] == rep_ref["failed_step"]
+        assert str(ei.value) == msg_ref
+    else:
+        assert abs(rep["failed_step"] - rep_ref["failed_step"]) <= 1
+
+
+def test_reference_time_levels_domain_error(gpu):
+    """run()'s repeated-subtraction time levels reach t < 0 at T=10, N=2000."""
+    p = W.make_problem(3, 0, nr=4, nv=3, ny=3, steps=2000)
+    p.time_levels = 0
+    with pytest.raises(hj.DomainError, match="discount: negative maturity"):
+        hj.Solver([p], mode="strict")
+
+
+def test_batch_run_driver(gpu, oracle):
+    probs = W.make_config(4, count=6, nr=24, nv=12, ny=12, steps=40)
+    prices, reps, grids = hj.batch_run(probs, devices=list(range(hj.device_count())),
+                                       mode="strict", grids=True)
+    off = 0
+    for q, p in enumerate(probs):
+        g_ref, _, _, _ = oracle.run(p)
+        g = grids[off:off + p.size].reshape(p.shape)
+        off += p.size
+        assert B.normwise_rel(g, g_ref) <= STRICT_TOL
+        assert abs(prices[q] - oracle.spot_price(p, g_ref)) <= TOL * abs(prices[q])
+        assert reps[q]["status"] == 0
