@@ -51,6 +51,7 @@ int32_t guarded(F&& f) {
         return HJMSV_OK;
     } catch (const Failure& e) {
         g_err = e.what();
+        cudaGetLastError();  // do not leak a sticky error into the next call
         return e.code;
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
@@ -743,10 +744,10 @@ int32_t hjmsv_thomas_batch(int32_t n, int32_t count, const double* lower, const 
         double *dl = dalloc<double>(m), *dd = dalloc<double>(m), *du = dalloc<double>(m);
         double *ds2 = dalloc<double>(count), *dr = dalloc<double>(m), *dsc = dalloc<double>(m);
         int* dfail = dalloc<int>(count);
-        auto cleanup = [&] {
-            for (void* q : {(void*)dl, (void*)dd, (void*)du, (void*)ds2, (void*)dr, (void*)dsc,
-                            (void*)dfail})
-                dfree(q);
+        auto cleanup = [&] {  // idempotent: pointers are cleared once freed
+            dfree(dl); dfree(dd); dfree(du); dfree(ds2); dfree(dr); dfree(dsc); dfree(dfail);
+            dl = dd = du = ds2 = dr = dsc = nullptr;
+            dfail = nullptr;
         };
         try {
             CK(cudaMemcpy(dl, lower, m * 8, cudaMemcpyHostToDevice));
