@@ -15,6 +15,8 @@
 //   k_fast_v   v-lines from the precomputed LU (stride ny, coalesced over k)
 //   k_fast_y   y-lines staged through shared memory + U += dU, Dirichlet, guard
 // Parity with the reference is checked to 1e-10 (tests/test_gpu_parity.py).
+#include <algorithm>
+
 #include "kernels_common.cuh"
 
 namespace hjmsv_b200 {
@@ -543,6 +545,774 @@ __global__ void __launch_bounds__(kYT) k_fast_y(BatchView v, int s) {
     if ((threadIdx.x & 31) == 0 && md) atomicMax(&st.maxdelta_bits, md);
 }
 
+// ===================================================================== v3
+// Pass A: explicit operator fused with the r-line elimination, 2.5D march.
+// A CTA of 32 x TJ threads owns the (j,k) columns j0..j0+TJ-1, k0..k0+31 and
+// marches i = 0..nr-1. U planes arrive as (TJ+2) x 34 halo slabs through a
+// cp.async ring (NB slabs, prefetch NB-3 ahead); the i-dependent factor tables
+// sit in shared memory (block-uniform broadcast reads). Each thread computes
+// dU0(i,j,k) from shared memory and immediately eliminates row i of its r-line
+// (projective pivots), storing c' -> C and d' -> D; the back-substitution then
+// streams C and D in reverse through per-thread rings.
+constexpr int kNB = 6;     // plane slabs in the ring
+constexpr int kSW = 34;    // slab row width: 32 columns + 2 halo
+
+__device__ __forceinline__ double explicit_smem(const BatchView& v, double react, double g1s,
+                                                double g4h, double g2s, double g5h, double g6h,
+                                                double g3s, const double* Sm, const double* S0,
+                                                const double* Sp, const double* S2, int c,
+                                                int i, int j, int k) {
+    // apply_operator (discretization.cpp:302-364) on a shared-memory stencil;
+    // Sm/S0/Sp = slabs of planes i-1, i, i+1 (S2 = plane 2, used at i = 0)
+    const double u0 = S0[c];
+    double acc = -react * u0;
+    if (i == 0) {
+        const double u1 = Sp[c];
+        if (v.r_order == 1)
+            acc = fma(2.0 * g4h, u1 - u0, acc);
+        else
+            acc = fma(g4h, fma(4.0, u1, -S2[c]) - 3.0 * u0, acc);
+    } else {
+        const double up = Sp[c], dn = Sm[c];
+        acc = fma(g1s, (up + dn) - 2.0 * u0, acc);
+        acc = fma(g4h, up - dn, acc);
+    }
+    if (j == 0) {
+        acc = fma(2.0 * g5h, S0[c + kSW] - u0, acc);
+    } else {
+        const double up = S0[c + kSW], dn = S0[c - kSW];
+        acc = fma(g2s, (up + dn) - 2.0 * u0, acc);
+        acc = fma(g5h, up - dn, acc);
+    }
+    if (k == 0) {
+        const double u1 = S0[c + 1];
+        if (v.y_order == 1)
+            acc = fma(2.0 * g6h, u1 - u0, acc);
+        else
+            acc = fma(g6h, fma(4.0, u1, -S0[c + 2]) - 3.0 * u0, acc);
+    } else {
+        acc = fma(g6h, S0[c + 1] - S0[c - 1], acc);
+    }
+    if (i > 0 && i < v.nr - 1 && j > 0 && j < v.nv - 1) {
+        const double cross = (Sp[c + kSW] - Sp[c - kSW]) - (Sm[c + kSW] - Sm[c - kSW]);
+        acc = fma(g3s, cross, acc);
+    }
+    return acc;
+}
+
+template <int TJ>
+__global__ void __launch_bounds__(32 * TJ) k_fast_rx(BatchView v, int s) {
+    extern __shared__ double sm[];
+    constexpr int NT = 32 * TJ;
+    constexpr int SP = (TJ + 2) * kSW;
+    const int p = blockIdx.y;
+    DevStatus& st = v.st[p];
+    if (st.fail_step) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) st.maxdelta_bits = 0ull;
+    const int nr = v.nr, nv = v.nv, ny = v.ny;
+    const int tiles_k = (ny + 31) >> 5;
+    const int jt = blockIdx.x / tiles_k;
+    const int j0 = jt * TJ, k0 = (blockIdx.x - jt * tiles_k) * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+    const int j = j0 + ty, k = k0 + tx;
+    const bool active = j < nv && k < ny;
+    const ProblemConst& pc = v.pc[p];
+    const size_t off = static_cast<size_t>(p) * v.N;
+    const double* __restrict__ U = v.U + off;
+    const int sr = nv * ny;
+
+    // shared memory: r tables [FR_COUNT][nr] | slab ring [kNB][SP] (reused by the back rings)
+    double* rt = sm;
+    double* ring = sm + FR_COUNT * nr;
+    const double* ftab = v.fast + static_cast<size_t>(p) * v.fast_stride;
+    for (int e = tid; e < FR_COUNT * nr; e += NT) rt[e] = ftab[e];
+    auto issue_slab = [&](int i) {
+        if (i >= nr) return;
+        double* dst = ring + (i % kNB) * SP;
+        const double* src = U + static_cast<size_t>(i) * sr;
+        for (int e = tid; e < SP; e += NT) {
+            const int rr = e / kSW, cc = e - rr * kSW;
+            const int jj = j0 - 1 + rr, kk = k0 - 1 + cc;
+            if (jj >= 0 && jj < nv && kk >= 0 && kk < ny) cp_async8(dst + e, src + jj * ny + kk);
+        }
+    };
+    for (int i = 0; i < kNB - 2; ++i) {
+        issue_slab(i);
+        cp_commit();
+    }
+
+    // per-column constants
+    const double* vt = ftab + FR_COUNT * nr;
+    const double* yt = vt + FV_COUNT * nv;
+    const Tab T = tables(v, p);
+    const int jc = active ? j : 0, kc = active ? k : 0;
+    const double vj = ld(vt + FV_V * nv + jc), g2s = ld(vt + FV_G2 * nv + jc);
+    const double g5h = ld(vt + FV_G5 * nv + jc), g3v = ld(vt + FV_G3 * nv + jc);
+    const double yk = ld(T.yz + kc), s6 = ld(yt + FY_S6 * ny + kc), t6 = ld(yt + FY_T6 * ny + kc);
+    const double th = pc.theta_dt, dtm = pc.dt;
+    const double c4 = step_row(v, p, s)[ST_C4];
+    const double* step = step_row(v, p, s);
+    // Dirichlet faces of this column (precedence r_max > y_max > v_max > r_min > y_min > v_min)
+    const bool rmaxD = pc.rule[F_RMAX] == RULE_DIRICHLET, rminD = pc.rule[F_RMIN] == RULE_DIRICHLET;
+    int hi = -1, lo = -1;
+    if (k == ny - 1 && pc.rule[F_YMAX] == RULE_DIRICHLET) hi = F_YMAX;
+    else if (j == nv - 1 && pc.rule[F_VMAX] == RULE_DIRICHLET) hi = F_VMAX;
+    if (k == 0 && pc.rule[F_YMIN] == RULE_DIRICHLET) lo = F_YMIN;
+    else if (j == 0 && pc.rule[F_VMIN] == RULE_DIRICHLET) lo = F_VMIN;
+    const bool solve = active && hi < 0 && lo < 0;  // !is_dirichlet(1,j,k) (solver.cpp:127)
+    const int c = (ty + 1) * kSW + tx + 1;
+    double* __restrict__ Dc = v.D + off + static_cast<size_t>(j) * ny + k;
+    double* __restrict__ Cc = v.C + off + static_cast<size_t>(j) * ny + k;
+
+    // elimination state
+    double dp = 0.0, pm1 = 1.0, pm2 = 1.0, uprev = 0.0;
+    double r0 = 0.0, d0 = 1.0, u0 = 0.0, s20 = 0.0;   // row 0 until the fold resolves
+    double r1 = 0.0, l1 = 0.0, d1 = 1.0, u1 = 0.0;    // row 1 when the fold needs row 2
+    int pending = 0;                                   // rows buffered before elimination
+    bool failed = false;
+    auto elim = [&](int i, double r, double l, double d, double u) {
+        if (failed) return;
+        if (i == 0) {
+            if (fabs(d) < 1e-300) {
+                record_pivot(st, s, 0, j * ny + k, 0);
+                failed = true;
+                return;
+            }
+            const double rp = frcp(d);
+            dp = r * rp;
+            Cc[0] = u * rp;
+            Dc[0] = dp;
+            pm2 = 1.0;
+            pm1 = d;
+            uprev = u;
+            return;
+        }
+        if (i == nr - 1 && l == 0.0 && d == 1.0) {  // Dirichlet identity row
+            dp = r;
+            Dc[static_cast<size_t>(i) * sr] = dp;
+            return;
+        }
+        const double P = fma(d, pm1, -(l * uprev) * pm2);
+        const double rp = pm1 * frcp(P);
+        if (fabs(rp) > 1e300) {  // |pivot| < 1e-300 (solver.cpp:49-52)
+            record_pivot(st, s, 0, j * ny + k, i);
+            failed = true;
+            return;
+        }
+        dp = fma(-l * rp, dp, r * rp);
+        Cc[static_cast<size_t>(i) * sr] = u * rp;
+        Dc[static_cast<size_t>(i) * sr] = dp;
+        pm2 = pm1;
+        pm1 = P;
+        uprev = u;
+        if ((i & 15) == 0) {
+            const double sc = pow2_scale(pm1);
+            pm1 *= sc;
+            pm2 *= sc;
+        }
+    };
+
+    for (int i = 0; i < nr; ++i) {
+        __syncthreads();  // slab i-2 is free for reuse
+        issue_slab(i + kNB - 2);
+        cp_commit();
+        if (i == 0)
+            cp_wait<0>();
+        else
+            cp_wait<kNB - 3>();
+        __syncthreads();
+        if (!active) continue;
+        const double* S0 = ring + (i % kNB) * SP;
+        const double* Sm = ring + ((i + kNB - 1) % kNB) * SP;
+        const double* Sp = ring + ((i + 1) % kNB) * SP;
+        const double* S2 = ring + (2 % kNB) * SP;
+        // Dirichlet node? (dirichlet_value precedence, discretization.cpp:172-192)
+        int face = -1;
+        if (i == nr - 1 && rmaxD) face = F_RMAX;
+        else if (hi >= 0) face = hi;
+        else if (i == 0 && rminD) face = F_RMIN;
+        else face = lo;
+        double rhs, l = 0.0, d = 1.0, u = 0.0, s2 = 0.0;
+        if (face >= 0) {
+            rhs = face_value(pc, step, T, face, i, k) - S0[c];  // solver.cpp:111-116
+        } else {
+            const double a_i = rt[FR_A * nr + i];
+            const double g1s = rt[FR_G1 * nr + i] * vj;
+            const double g4h = fma(c4, rt[FR_G4C * nr + i],
+                                   fma(rt[FR_G4Q * nr + i], yk,
+                                       fma(rt[FR_G4V * nr + i], vj, rt[FR_G4P * nr + i])));
+            const double g6h = fma(a_i * vj, s6, t6);
+            const double g3s = rt[FR_G3 * nr + i] * g3v;
+            rhs = dtm * explicit_smem(v, rt[FR_REACT * nr + i], g1s, g4h, g2s, g5h, g6h, g3s, Sm,
+                                      S0, Sp, S2, c, i, j, k);
+            if (i == 0) {  // degenerate row (discretization.cpp:207-218)
+                if (v.r_order == 1) {
+                    d = fma(2.0 * th, g4h, 1.0);
+                    u = -2.0 * th * g4h;
+                } else {
+                    d = fma(3.0 * th, g4h, 1.0);
+                    u = -4.0 * th * g4h;
+                    s2 = th * g4h;
+                }
+            } else {
+                const double w2 = th * g1s, w1 = th * g4h;
+                l = w1 - w2;
+                d = fma(2.0, w2, 1.0);
+                u = -(w2 + w1);
+            }
+        }
+        if (!solve) {
+            Dc[static_cast<size_t>(i) * sr] = rhs;
+            continue;
+        }
+        if (i == 0) {
+            r0 = rhs; d0 = d; u0 = u; s20 = s2;
+            pending = 1;
+            continue;
+        }
+        if (pending == 1) {  // i == 1: resolve the (0,2) fold (solver.cpp:28-40)
+            if (s20 != 0.0 && nr > 2) {
+                if (fabs(u) > 1e-300) {
+                    const double f = s20 / u;
+                    d0 = fma(-f, l, d0);
+                    u0 = fma(-f, d, u0);
+                    r0 = fma(-f, rhs, r0);
+                } else {  // needs rhs of row 2: keep row 1 buffered
+                    r1 = rhs; l1 = l; d1 = d; u1 = u;
+                    pending = 2;
+                    continue;
+                }
+            }
+            elim(0, r0, 0.0, d0, u0);
+            elim(1, rhs, l, d, u);
+            pending = 0;
+            continue;
+        }
+        if (pending == 2) {  // i == 2, vanishing coupling: lag s2 on rhs[2]
+            r0 = fma(-s20, rhs, r0);
+            elim(0, r0, 0.0, d0, u0);
+            elim(1, r1, l1, d1, u1);
+            pending = 0;
+        }
+        elim(i, rhs, l, d, u);
+    }
+    cp_wait<0>();
+    __syncthreads();
+    if (!solve || failed) return;
+    // back-substitution (solver.cpp:56) over rows nr-2..0
+    const LineStream cs{ring, NT, tid, Cc, sr, nr - 1, -1};
+    const LineStream ds{ring + kRD * NT, NT, tid, Dc, sr, nr - 1, -1};
+    for (int q = 0; q < kRD - 1; ++q) {
+        cs.issue(q);
+        ds.issue(q);
+        cp_commit();
+    }
+    double x = dp;
+    for (int q = 0; q < nr - 1; ++q) {
+        cs.issue(q + kRD - 1);
+        ds.issue(q + kRD - 1);
+        cp_commit();
+        cp_wait<kRD - 1>();
+        x = fma(-*cs.slot(q), x, *ds.slot(q));
+        Dc[static_cast<size_t>(nr - 2 - q) * sr] = x;
+    }
+}
+
+// Pass B: one CTA per i-plane (v,y) held in shared memory (pitch ny+1):
+// v-sweep from the precomputed LU (thread per column k), y-sweep (thread per
+// row j, projective pivots, c' in a transposed global scratch streamed back
+// through per-thread rings), then U += dU, Dirichlet re-impose, max|dU| and
+// the guard over the plane (solver.cpp:136-176).
+constexpr int kPT = 256;
+
+__global__ void __launch_bounds__(kPT) k_fast_plane(BatchView v, int s) {
+    extern __shared__ double sm[];
+    const int p = blockIdx.y;
+    const int i = blockIdx.x;
+    DevStatus& st = v.st[p];
+    if (st.fail_step) return;
+    const int nr = v.nr, nv = v.nv, ny = v.ny;
+    const int pitch = ny + 1;
+    double* tile = sm;                         // [nv][ny+1]
+    double* vlu = tile + nv * pitch;           // L, CP, RP [3][nv]
+    double* ys = vlu + 3 * nv;                 // S6, T6 [2][ny]
+    double* ring = ys + 2 * ny;                // [kRD][nv] back rings of the y-sweep
+    const size_t off = static_cast<size_t>(p) * v.N;
+    const size_t pbase = off + static_cast<size_t>(i) * nv * ny;
+    const int cnt = nv * ny;
+    for (int e = threadIdx.x; e < cnt; e += kPT) {
+        const int jj = e / ny, kk = e - jj * ny;
+        cp_async8(tile + jj * pitch + kk, v.D + pbase + e);
+    }
+    cp_commit();
+    const double* ftab = v.fast + static_cast<size_t>(p) * v.fast_stride;
+    const double* vt = ftab + FR_COUNT * v.nr;
+    const double* yt = vt + FV_COUNT * nv;
+    for (int e = threadIdx.x; e < nv; e += kPT) {
+        vlu[e] = vt[FV_L * nv + e];
+        vlu[nv + e] = vt[FV_CP * nv + e];
+        vlu[2 * nv + e] = vt[FV_RP * nv + e];
+    }
+    for (int e = threadIdx.x; e < ny; e += kPT) {
+        ys[e] = yt[FY_S6 * ny + e];
+        ys[ny + e] = yt[FY_T6 * ny + e];
+    }
+    const ProblemConst& pc = v.pc[p];
+    const double th = pc.theta_dt;
+    const double a_i = ftab[FR_A * nr + i], react = ftab[FR_REACT * nr + i];
+    cp_wait<0>();
+    __syncthreads();
+    const bool plane_dir = (i == 0 && pc.rule[F_RMIN] == RULE_DIRICHLET) ||
+                           (i == nr - 1 && pc.rule[F_RMAX] == RULE_DIRICHLET);
+    // ---- v-sweep (solver.cpp:136-149): lines with !is_dirichlet(i,1,k)
+    if (!plane_dir) {
+        for (int kk = threadIdx.x; kk < ny; kk += kPT) {
+            const bool kd = (kk == 0 && pc.rule[F_YMIN] == RULE_DIRICHLET) ||
+                            (kk == ny - 1 && pc.rule[F_YMAX] == RULE_DIRICHLET);
+            if (kd) continue;
+            double* x = tile + kk;
+            double dp = 0.0;
+            bool ok = true;
+            for (int jj = 0; jj < nv; ++jj) {
+                const double rp = vlu[2 * nv + jj];
+                if (isnan(rp)) {
+                    record_pivot(st, s, 1, i * ny + kk, jj);
+                    ok = false;
+                    break;
+                }
+                const double r = x[jj * pitch];
+                dp = (jj == 0 ? r : fma(-vlu[jj], dp, r)) * rp;
+                x[jj * pitch] = dp;
+            }
+            if (!ok) continue;
+            double xv = dp;
+            for (int jj = nv - 2; jj >= 0; --jj) {
+                xv = fma(-vlu[nv + jj], xv, x[jj * pitch]);
+                x[jj * pitch] = xv;
+            }
+        }
+    }
+    __syncthreads();
+    // ---- y-sweep (solver.cpp:151-161): lines with !is_dirichlet(i,j,1)
+    const double dint = fma(th, react, 1.0);
+    const double* vz = ftab + FR_COUNT * nr + FV_V * nv;
+    double* __restrict__ cplane = v.C + pbase;  // c'_k of line j at cplane[k*nv + j]
+    if (!plane_dir) {
+        for (int jj = threadIdx.x; jj < nv; jj += kPT) {
+            const bool jd = (jj == 0 && pc.rule[F_VMIN] == RULE_DIRICHLET) ||
+                            (jj == nv - 1 && pc.rule[F_VMAX] == RULE_DIRICHLET);
+            if (jd) continue;
+            double* x = tile + jj * pitch;
+            double* cs = cplane + jj;
+            const double h1 = a_i * vz[jj];
+            double d0 = 1.0, u0 = 0.0, s20 = 0.0;
+            if (pc.rule[F_YMIN] != RULE_DIRICHLET) {  // row 0 (discretization.cpp:280-289)
+                const double g6h = fma(h1, ys[0], ys[ny]);
+                if (v.y_order == 1) {
+                    d0 = fma(th, fma(2.0, g6h, react), 1.0);
+                    u0 = -2.0 * th * g6h;
+                } else {
+                    d0 = fma(th, fma(3.0, g6h, react), 1.0);
+                    u0 = -4.0 * th * g6h;
+                    s20 = th * g6h;
+                }
+            }
+            double r0 = x[0];
+            if (s20 != 0.0 && ny > 2) {
+                const double l1 = th * fma(h1, ys[1], ys[ny + 1]);
+                const double u1 = -l1;
+                if (fabs(u1) > 1e-300) {
+                    const double f = s20 / u1;
+                    d0 = fma(-f, l1, d0);
+                    u0 = fma(-f, dint, u0);
+                    r0 = fma(-f, x[1], r0);
+                } else {
+                    r0 = fma(-s20, x[2], r0);
+                }
+            }
+            if (fabs(d0) < 1e-300) {
+                record_pivot(st, s, 2, i * nv + jj, 0);
+                continue;
+            }
+            double rp = frcp(d0);
+            double dp = r0 * rp;
+            cs[0] = u0 * rp;
+            x[0] = dp;
+            double pm2 = 1.0, pm1 = d0, uprev = u0;
+            bool ok = true;
+            for (int kk = 1; kk < ny - 1; ++kk) {
+                const double l = th * fma(h1, ys[kk], ys[ny + kk]);
+                const double P = fma(dint, pm1, (l * uprev) * pm2 * -1.0);
+                rp = pm1 * frcp(P);
+                if (fabs(rp) > 1e300) {
+                    record_pivot(st, s, 2, i * nv + jj, kk);
+                    ok = false;
+                    break;
+                }
+                dp = fma(-l * rp, dp, x[kk] * rp);
+                cs[static_cast<size_t>(kk) * nv] = -l * rp;
+                x[kk] = dp;
+                pm2 = pm1;
+                pm1 = P;
+                uprev = -l;
+                if ((kk & 15) == 0) {
+                    const double sc = pow2_scale(pm1);
+                    pm1 *= sc;
+                    pm2 *= sc;
+                }
+            }
+            if (!ok) continue;
+            // row ny-1 is the y_max identity row: x[ny-1] keeps its rhs
+            const LineStream bk{ring, nv, jj, cs, nv, ny - 1, -1};
+            bk.prologue();
+            double xv = x[ny - 1];
+            for (int q = 0; q < ny - 1; ++q) {
+                const int kk = ny - 2 - q;
+                xv = fma(-bk.next(q), xv, x[kk]);
+                x[kk] = xv;
+            }
+            cp_wait<0>();
+        }
+    }
+    __syncthreads();
+    if (st.fail_step) return;  // the reference throws before the update
+    // ---- U += dU, max|dU|, Dirichlet re-impose, guard (solver.cpp:163-176)
+    const double* step = step_row(v, p, s);
+    const Tab T = tables(v, p);
+    unsigned long long md = 0ull;
+    double* __restrict__ Up = v.U + pbase;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < cnt; e += kPT) {
+        const int jj = e / ny, kk = e - jj * ny;
+        const double dq = tile[jj * pitch + kk];
+        double un = Up[e] + dq;
+        const double ad = fabs(dq);
+        if (ad > 0.0) {
+            const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(ad));
+            md = b > md ? b : md;
+        }
+        const int face = dirichlet_face(v, pc, i, jj, kk);
+        if (face >= 0) un = face_value(pc, step, T, face, i, kk);
+        Up[e] = un;
+        const unsigned long long flat = static_cast<unsigned long long>(pbase - off + e);
+        if (!isfinite(un)) {
+            atomicMin(&st.nonfinite_first, flat);
+            mark_fail(st, s + 1, HJMSV_NONFINITE);
+        } else if (fabs(un) > pc.bound) {
+            atomicMin(&st.diverge_first, flat);
+            mark_fail(st, s + 1, HJMSV_DIVERGED);
+        }
+    }
+    md = warp_max(md);
+    if ((threadIdx.x & 31) == 0 && md) atomicMax(&st.maxdelta_bits, md);
+}
+
+// ================================================================ pass A v4
+// Explicit operator fused with a SEGMENTED r-line solve (partition method).
+// Block = LANES consecutive k (same j) x S segments of M rows (S = ceil(nr/M)).
+// Thread (k, s) computes dU0 for rows a..a+m-1 of column (j,k) from U (rolling
+// register window over i; k+-1 through shuffles) and eliminates each row as it
+// is produced, for three right-hand sides sharing one factorisation:
+//     T y = r,   T alpha = -l_a e_0,   T beta = -u_{a+m-1} e_{m-1},
+// so x_i = y_i + alpha_i x_{a-1} + beta_i x_{a+m}. The end rows of all segments
+// form a reduced system in (x_last(s), x_first(s+1)), solved per line by one
+// thread in shared memory; each thread then writes x_i = dU1 for its rows.
+// Everything between the U loads and the dU1 stores stays in registers (no
+// c'/d' scratch traffic). The elimination order differs from the reference's
+// sequential Thomas (the north star's allowed source of difference); local and
+// reduced pivots replace the global ones in the singular-pivot check.
+template <int M, int LANES>
+__global__ void __launch_bounds__(512) k_fast_rseg(BatchView v, int s) {
+    extern __shared__ double red[];  // [8][S][LANES]: yF aF bF yL aL bL | p q
+    const int p = blockIdx.y;
+    DevStatus& st = v.st[p];
+    if (st.fail_step) return;
+    const int nr = v.nr, nv = v.nv, ny = v.ny;
+    const int S = blockDim.y;
+    const int tx = threadIdx.x, sg = threadIdx.y;
+    if (blockIdx.x == 0 && tx == 0 && sg == 0) st.maxdelta_bits = 0ull;
+    const int tiles_k = (ny + LANES - 1) / LANES;
+    const int j = blockIdx.x / tiles_k;
+    const int k = (blockIdx.x - j * tiles_k) * LANES + tx;
+    const bool active = k < ny;
+    const int kc = active ? k : ny - 1;
+    const int a = sg * M;
+    const int m = min(M, nr - a);
+    const ProblemConst& pc = v.pc[p];
+    const size_t off = static_cast<size_t>(p) * v.N;
+    const int sr = nv * ny;
+    const double* ftab = v.fast + static_cast<size_t>(p) * v.fast_stride;
+    const double* rt = ftab;                  // r tables [FR_COUNT][nr]
+    const double* vt = ftab + FR_COUNT * nr;  // v tables
+    const double* yt = vt + FV_COUNT * nv;    // y tables
+    const Tab T = tables(v, p);
+    const double vj = ld(vt + FV_V * nv + j), g2s = ld(vt + FV_G2 * nv + j);
+    const double g5h = ld(vt + FV_G5 * nv + j), g3v = ld(vt + FV_G3 * nv + j);
+    const double yk = ld(T.yz + kc), vs6 = vj * ld(yt + FY_S6 * ny + kc);
+    const double t6 = ld(yt + FY_T6 * ny + kc);
+    const double th = pc.theta_dt, dtm = pc.dt;
+    const double* step = step_row(v, p, s);
+    const double c4 = step[ST_C4];
+    const bool rmaxD = pc.rule[F_RMAX] == RULE_DIRICHLET, rminD = pc.rule[F_RMIN] == RULE_DIRICHLET;
+    int hi = -1, lo = -1;  // Dirichlet faces of this column, precedence order
+    if (k == ny - 1 && pc.rule[F_YMAX] == RULE_DIRICHLET) hi = F_YMAX;
+    else if (j == nv - 1 && pc.rule[F_VMAX] == RULE_DIRICHLET) hi = F_VMAX;
+    if (k == 0 && pc.rule[F_YMIN] == RULE_DIRICHLET) lo = F_YMIN;
+    else if (j == 0 && pc.rule[F_VMIN] == RULE_DIRICHLET) lo = F_VMIN;
+    const bool solve = active && hi < 0 && lo < 0;  // !is_dirichlet(1,j,k) (solver.cpp:127)
+    const bool jlo = j > 0, jhi = j < nv - 1;
+    const double* col = v.U + off + static_cast<size_t>(j) * ny + kc;  // U(0, j, k)
+    double* dcol = v.D + off + static_cast<size_t>(j) * ny + kc;
+
+    // rolling window of U(i', j-1..j+1, k) for i' = i-1, i, i+1
+    auto load3 = [&](int ii, double& w0, double& w1, double& w2) {
+        if (ii < 0 || ii >= nr) {
+            w0 = w1 = w2 = 0.0;
+            return;
+        }
+        const double* q = col + static_cast<size_t>(ii) * sr;
+        w1 = __ldg(q);
+        w0 = jlo ? __ldg(q - ny) : 0.0;
+        w2 = jhi ? __ldg(q + ny) : 0.0;
+    };
+    double am0, am1, am2, a00, a01, a02, ap0, ap1, ap2;
+    load3(a - 1, am0, am1, am2);
+    load3(a, a00, a01, a02);
+    load3(a + 1, ap0, ap1, ap2);
+    double u2_0 = 0.0;  // U(2, j, k) for the one-sided r stencil at i = 0
+    if (a == 0 && nr > 2) u2_0 = __ldg(col + 2 * static_cast<size_t>(sr));
+
+    // elimination state: c'_r, y'_r, alpha'_r of the segment's rows
+    double cs[M], ys[M], as[M];
+    double cprev = 0.0, yprev = 0.0, aprev = 0.0;
+    double bLs = 0.0, yLs = 0.0, aLs = 0.0;  // end-row values at r = m-1
+    bool bad = false;
+    int bad_row = 0;
+    // row 0 of the line (segment 0): held until row 1 (or 2) resolves the fold
+    double h0r = 0.0, h0d = 1.0, h0u = 0.0, h0s = 0.0;
+    double h1r = 0.0, h1l = 0.0, h1d = 1.0, h1u = 0.0;
+    int hold = 0;
+
+    // eliminate row r (0-based in the segment) with coefficients (l, d, u)
+    auto elim = [&](int r, double rhs, double l, double d, double u) {
+        const double piv = r == 0 ? d : fma(-l, cprev, d);
+        if (fabs(piv) < 1e-300 && !bad) {
+            bad = true;
+            bad_row = a + r;
+        }
+        const double rp = frcp(piv);
+        const bool last = r == m - 1;
+        const double c = last ? 0.0 : u * rp;  // the last row's upper couples to x_{a+m}
+        const double yy = (r == 0 ? rhs : fma(-l, yprev, rhs)) * rp;
+        const double aa = (r == 0 ? -l : -l * aprev) * rp;
+        if (last) {
+            bLs = -u * rp;
+            yLs = yy;
+            aLs = aa;
+        }
+        cprev = c;
+        yprev = yy;
+        aprev = aa;
+        return c;
+    };
+
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+        const int i = a + r;
+        double kl = __shfl_up_sync(0xffffffffu, a01, 1, LANES);
+        double kr = __shfl_down_sync(0xffffffffu, a01, 1, LANES);
+        if (r < m) {
+            const double* q = col + static_cast<size_t>(i) * sr;
+            if (tx == 0) kl = k > 0 ? __ldg(q - 1) : 0.0;
+            if (tx == LANES - 1 || k == ny - 1) kr = k < ny - 1 ? __ldg(q + 1) : 0.0;
+            int face;
+            if (i == nr - 1 && rmaxD) face = F_RMAX;
+            else if (hi >= 0) face = hi;
+            else if (i == 0 && rminD) face = F_RMIN;
+            else face = lo;
+            double rhs, l = 0.0, d = 1.0, u = 0.0, s2 = 0.0;
+            if (face >= 0) {
+                rhs = face_value(pc, step, T, face, i, kc) - a01;  // solver.cpp:111-116
+            } else {
+                // dt*F(U) (apply_operator, discretization.cpp:302-364)
+                const double g1s = ld(rt + FR_G1 * nr + i) * vj;
+                const double g4h = fma(c4, ld(rt + FR_G4C * nr + i),
+                                       fma(ld(rt + FR_G4Q * nr + i), yk,
+                                           fma(ld(rt + FR_G4V * nr + i), vj,
+                                               ld(rt + FR_G4P * nr + i))));
+                const double g6h = fma(ld(rt + FR_A * nr + i), vs6, t6);
+                const double u0 = a01;
+                double acc = -ld(rt + FR_REACT * nr + i) * u0;
+                if (i == 0) {
+                    if (v.r_order == 1)
+                        acc = fma(2.0 * g4h, ap1 - u0, acc);
+                    else
+                        acc = fma(g4h, fma(4.0, ap1, -u2_0) - 3.0 * u0, acc);
+                } else {
+                    acc = fma(g1s, (ap1 + am1) - 2.0 * u0, acc);
+                    acc = fma(g4h, ap1 - am1, acc);
+                }
+                if (j == 0) {
+                    acc = fma(2.0 * g5h, a02 - u0, acc);
+                } else {
+                    acc = fma(g2s, (a02 + a00) - 2.0 * u0, acc);
+                    acc = fma(g5h, a02 - a00, acc);
+                }
+                if (k == 0) {
+                    if (v.y_order == 1)
+                        acc = fma(2.0 * g6h, kr - u0, acc);
+                    else
+                        acc = fma(g6h, fma(4.0, kr, -__ldg(q + 2)) - 3.0 * u0, acc);
+                } else {
+                    acc = fma(g6h, kr - kl, acc);
+                }
+                if (i > 0 && i < nr - 1 && jlo && jhi)
+                    acc = fma(ld(rt + FR_G3 * nr + i) * g3v, (ap2 - ap0) - (am2 - am0), acc);
+                rhs = dtm * acc;
+                if (i == 0) {  // degenerate row (discretization.cpp:207-218)
+                    if (v.r_order == 1) {
+                        d = fma(2.0 * th, g4h, 1.0);
+                        u = -2.0 * th * g4h;
+                    } else {
+                        d = fma(3.0 * th, g4h, 1.0);
+                        u = -4.0 * th * g4h;
+                        s2 = th * g4h;
+                    }
+                } else {
+                    const double w2 = th * g1s, w1 = th * g4h;
+                    l = w1 - w2;
+                    d = fma(2.0, w2, 1.0);
+                    u = -(w2 + w1);
+                }
+            }
+            am0 = a00; am1 = a01; am2 = a02;  // advance the window
+            a00 = ap0; a01 = ap1; a02 = ap2;
+            load3(i + 2, ap0, ap1, ap2);
+            if (!solve) {
+                if (active) dcol[static_cast<size_t>(i) * sr] = rhs;
+            } else if (a == 0 && r == 0) {
+                h0r = rhs; h0d = d; h0u = u; h0s = s2;  // wait for row 1 (fold)
+                hold = 1;
+            } else if (a == 0 && r == 1) {
+                if (h0s != 0.0 && nr > 2 && !(fabs(u) > 1e-300)) {
+                    h1r = rhs; h1l = l; h1d = d; h1u = u;  // fold needs rhs of row 2
+                    hold = 2;
+                } else {
+                    if (h0s != 0.0 && nr > 2) {  // fold (0,2) against row 1 (solver.cpp:28-40)
+                        const double f = h0s / u;
+                        h0d = fma(-f, l, h0d);
+                        h0u = fma(-f, d, h0u);
+                        h0r = fma(-f, rhs, h0r);
+                    }
+                    cs[0] = elim(0, h0r, 0.0, h0d, h0u);
+                    ys[0] = yprev;
+                    as[0] = aprev;
+                    cs[1] = elim(1, rhs, l, d, u);
+                    ys[1] = yprev;
+                    as[1] = aprev;
+                    hold = 0;
+                }
+            } else if (a == 0 && r == 2 && hold == 2) {
+                h0r = fma(-h0s, rhs, h0r);  // vanishing coupling: lag s2 on rhs[2]
+                cs[0] = elim(0, h0r, 0.0, h0d, h0u);
+                ys[0] = yprev;
+                as[0] = aprev;
+                cs[1] = elim(1, h1r, h1l, h1d, h1u);
+                ys[1] = yprev;
+                as[1] = aprev;
+                cs[2] = elim(2, rhs, l, d, u);
+                ys[2] = yprev;
+                as[2] = aprev;
+                hold = 0;
+            } else {
+                cs[r] = elim(r, rhs, l, d, u);
+                ys[r] = yprev;
+                as[r] = aprev;
+            }
+        }
+    }
+    // local back-substitution of y and alpha (beta follows in the final pass)
+    double yF = 0.0, aF = 0.0, bF = 0.0;
+    if (solve) {
+        double yn = yLs, an = aLs, bn = bLs;
+#pragma unroll
+        for (int r = M - 2; r >= 0; --r) {
+            if (r < m - 1) {
+                yn = fma(-cs[r], yn, ys[r]);
+                an = fma(-cs[r], an, as[r]);
+                bn = -cs[r] * bn;
+                ys[r] = yn;
+                as[r] = an;
+            }
+        }
+        yF = m > 1 ? yn : yLs;
+        aF = m > 1 ? an : aLs;
+        bF = m > 1 ? bn : bLs;
+        if (bad) record_pivot(st, s, 0, j * ny + k, bad_row);
+    }
+    const int L = LANES;
+    const int SL = S * L;
+    const int idx = sg * L + tx;
+    double* R = red;
+    if (solve) {
+        R[0 * SL + idx] = yF;
+        R[1 * SL + idx] = aF;
+        R[2 * SL + idx] = bF;
+        R[3 * SL + idx] = yLs;
+        R[4 * SL + idx] = aLs;
+        R[5 * SL + idx] = bLs;
+    }
+    __syncthreads();
+    if (sg == 0 && solve && S > 1) {
+        // reduced system in p_s = x_last(s), q_s = x_first(s+1), s = 0..S-2:
+        //   p_s = yL_s + aL_s p_{s-1} + bL_s q_s
+        //   q_s = yF_{s+1} + aF_{s+1} p_s + bF_{s+1} q_{s+1}
+        double Pp = 0.0, Pq = 0.0;
+        for (int q = 0; q < S - 1; ++q) {
+            const int c0 = q * L + tx, c1 = c0 + L;
+            const double aL = R[4 * SL + c0];
+            const double A = fma(aL, Pp, R[3 * SL + c0]);
+            const double B = fma(aL, Pq, R[5 * SL + c0]);
+            const double aFn = R[1 * SL + c1];
+            const double den = fma(-aFn, B, 1.0);
+            if (fabs(den) < 1e-300) record_pivot(st, s, 0, j * ny + k, (q + 1) * M);
+            const double inv = frcp(den);
+            const double Qc = fma(aFn, A, R[0 * SL + c1]) * inv;
+            const double Qd = R[2 * SL + c1] * inv;
+            Pp = fma(B, Qc, A);
+            Pq = B * Qd;
+            R[6 * SL + c0] = Qc;
+            R[7 * SL + c0] = Qd;
+            R[3 * SL + c0] = Pp;
+            R[4 * SL + c0] = Pq;
+        }
+        double qn = 0.0;  // q_{S-1} does not exist
+        for (int q = S - 2; q >= 0; --q) {
+            const int c0 = q * L + tx;
+            const double qs = fma(R[7 * SL + c0], qn, R[6 * SL + c0]);
+            const double ps = fma(R[4 * SL + c0], qn, R[3 * SL + c0]);
+            R[6 * SL + c0] = ps;  // p_s = x_last(s)
+            R[7 * SL + c0] = qs;  // q_s = x_first(s+1)
+            qn = qs;
+        }
+    }
+    __syncthreads();
+    if (!solve) return;
+    const double left = sg > 0 ? R[6 * SL + idx - L] : 0.0;
+    const double right = sg < S - 1 ? R[7 * SL + idx] : 0.0;
+    // x_r = y_r + alpha_r x_{a-1} + beta_r x_{a+m}, beta recomputed downwards
+    double b = bLs;
+#pragma unroll
+    for (int r = M - 1; r >= 0; --r) {
+        if (r < m) {
+            if (r < m - 1) b = -cs[r] * b;
+            const double yv = r == m - 1 ? yLs : ys[r];
+            const double av = r == m - 1 ? aLs : as[r];
+            dcol[static_cast<size_t>(a + r) * sr] = fma(b, right, fma(av, left, yv));
+        }
+    }
+}
+
 }  // namespace
 
 bool fast_supported(int nr, int nv, int ny) {
@@ -552,10 +1322,33 @@ bool fast_supported(int nr, int nv, int ny) {
 
 int fast_stride(int nr, int nv, int ny) { return fast_table_stride(nr, nv, ny); }
 
+namespace {
+constexpr int kRXTJ = 2;
+size_t rx_smem(const BatchView& v) {
+    constexpr int NT = 32 * kRXTJ, SP = (kRXTJ + 2) * kSW;
+    const size_t ring = std::max<size_t>(static_cast<size_t>(kNB) * SP, 2ull * kRD * NT);
+    return (static_cast<size_t>(FR_COUNT) * v.nr + ring) * sizeof(double);
+}
+size_t plane_smem(const BatchView& v) {
+    return (static_cast<size_t>(v.nv) * (v.ny + 1) + 3 * v.nv + 2 * v.ny +
+            static_cast<size_t>(kRD) * v.nv) * sizeof(double);
+}
+size_t y_smem(const BatchView& v) {
+    return (static_cast<size_t>(kTL) * (v.ny + 1) + kRD * kTL) * sizeof(double);
+}
+constexpr size_t kSmemCap = 220 * 1024;
+constexpr int kSegM = 8;  // rows per r-segment
+size_t seg_smem(int S, int lanes) { return 8ull * S * lanes * sizeof(double); }
+}  // namespace
+
 void fast_prepare(const BatchView& v, cudaStream_t) {
-    const size_t ysm = (static_cast<size_t>(kTL) * (v.ny + 1) + kRD * kTL) * sizeof(double);
     cudaFuncSetAttribute(k_fast_y, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(ysm));
+                         static_cast<int>(y_smem(v)));
+    cudaFuncSetAttribute(k_fast_rx<kRXTJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(rx_smem(v)));
+    if (plane_smem(v) <= kSmemCap)
+        cudaFuncSetAttribute(k_fast_plane, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(plane_smem(v)));
 }
 
 void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launches,
@@ -564,23 +1357,36 @@ void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launch
         if (launches) ++*launches;
         if (hook && hook->after) hook->after(hook->ctx, idx, name, bytes);
     };
-    // algorithmic bytes/point of each launch: read U + write dU0 (16) | read + write
-    // the line (16) | read + write the line (16) | read dU, read U, write U (24)
-    const unsigned npts = static_cast<unsigned>((v.N + 255) / 256);
-    k_fast_explicit<<<dim3(npts, v.P), 256, 0, stream>>>(v, s);
-    mark(0, "fast_explicit", 16.0);
-    const int rt = 64;
-    k_fast_r<<<dim3((v.nv * v.ny + rt - 1) / rt, v.P), rt, 2 * kRD * rt * sizeof(double),
-               stream>>>(v, s);
-    mark(1, "fast_sweep_r", 16.0);
-    const int vt = 128;
-    k_fast_v<<<dim3((v.nr * v.ny + vt - 1) / vt, v.P), vt, kRD * vt * sizeof(double), stream>>>(
-        v, s);
-    mark(2, "fast_sweep_v", 16.0);
-    const int lines = v.nr * v.nv;
-    const size_t ysm = (static_cast<size_t>(kTL) * (v.ny + 1) + kRD * kTL) * sizeof(double);
-    k_fast_y<<<dim3((lines + kTL - 1) / kTL, v.P), kYT, ysm, stream>>>(v, s);
-    mark(3, "fast_sweep_y_update", 24.0);
+    // algorithmic bytes per point of each launch (SURVEY §8d accounting):
+    //   pass A  read U, write dU1                         16
+    //   pass B  read dU1, read U, write U                 24  (v + y + update fused)
+    const int S = (v.nr + kSegM - 1) / kSegM;
+    if (S <= 16) {
+        const int tiles = v.nv * ((v.ny + 31) / 32);
+        k_fast_rseg<kSegM, 32><<<dim3(tiles, v.P), dim3(32, S), seg_smem(S, 32), stream>>>(v, s);
+    } else if (S <= 32) {
+        const int tiles = v.nv * ((v.ny + 15) / 16);
+        k_fast_rseg<kSegM, 16><<<dim3(tiles, v.P), dim3(16, S), seg_smem(S, 16), stream>>>(v, s);
+    } else if (S <= 64) {
+        const int tiles = v.nv * ((v.ny + 7) / 8);
+        k_fast_rseg<kSegM, 8><<<dim3(tiles, v.P), dim3(8, S), seg_smem(S, 8), stream>>>(v, s);
+    } else {
+        const int tiles = ((v.nv + kRXTJ - 1) / kRXTJ) * ((v.ny + 31) / 32);
+        k_fast_rx<kRXTJ><<<dim3(tiles, v.P), dim3(32, kRXTJ), rx_smem(v), stream>>>(v, s);
+    }
+    mark(0, "fast_explicit_r", 16.0);
+    if (plane_smem(v) <= kSmemCap) {
+        k_fast_plane<<<dim3(v.nr, v.P), kPT, plane_smem(v), stream>>>(v, s);
+        mark(1, "fast_plane_vy_update", 24.0);
+    } else {
+        const int vt = 128;
+        k_fast_v<<<dim3((v.nr * v.ny + vt - 1) / vt, v.P), vt, kRD * vt * sizeof(double),
+                   stream>>>(v, s);
+        mark(1, "fast_sweep_v", 16.0);
+        const int lines = v.nr * v.nv;
+        k_fast_y<<<dim3((lines + kTL - 1) / kTL, v.P), kYT, y_smem(v), stream>>>(v, s);
+        mark(2, "fast_sweep_y_update", 24.0);
+    }
 }
 
 void fast_explicit(const BatchView& v, int s, cudaStream_t stream) {
