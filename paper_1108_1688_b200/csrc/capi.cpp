@@ -296,6 +296,14 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
     v.steps = h->steps;
     v.st = h->st;
     v.apply_only = ov && ov->apply_only ? 1 : 0;
+    v.dmask = 0;
+    for (int f = 0; f < 6; ++f) {
+        const bool dir = pcs[0].rule[f] == RULE_DIRICHLET;
+        for (int p = 1; p < count; ++p)
+            if ((pcs[p].rule[f] == RULE_DIRICHLET) != dir)
+                throw std::invalid_argument("batched problems must share face rules");
+        if (dir) v.dmask |= 1 << f;
+    }
     h->stage = ov != nullptr;
     if (mode == HJMSV_MODE_FAST) {
         v.fast_stride = fast_stride(h->nr, h->nv, h->ny);

@@ -66,22 +66,28 @@ struct BatchView {
     const double* fast;   // [P][fast_stride] derived factor tables (FAST mode)
     int fast_stride;
     int apply_only;       // stage mode: D = F(U), Dirichlet nodes 0 (apply_operator)
+    int dmask;            // bit f set when face f is Dirichlet (uniform across the batch)
 };
 
 inline int axes_stride(int nr, int nv, int ny) { return 5 * nr + 3 * nv + 3 * ny; }
 
-// FAST-mode factor tables per problem (host-built, lowering.cpp): the
-// separable pieces of g1..g6 (discretization.cpp:56-72) with the stencil
-// 1/dx factors folded in, plus the v-line LU, which depends on j only.
-//   g1/dxr^2      = G1[i]*v_j            g4/(2dxr) = c4*G4C[i] + G4P[i] + G4Q[i]*y_k + G4V[i]*v_j
-//   g3/(4dxr dxv) = G3[i]*G3V[j]         g2/dxv^2  = G2[j],  g5/(2dxv) = G5[j]
-//   g6/(2dxy)     = a_i v_j S6[k] + T6[k]           reaction = REACT[i]
-enum FastR : int { FR_G1 = 0, FR_G4C, FR_G4P, FR_G4Q, FR_G4V, FR_G3, FR_REACT, FR_A, FR_COUNT };
-enum FastV : int { FV_V = 0, FV_G2, FV_G5, FV_G3, FV_L, FV_CP, FV_RP, FV_COUNT };
-enum FastY : int { FY_S6 = 0, FY_T6, FY_COUNT };
-inline int fast_table_stride(int nr, int nv, int ny) {
-    return FR_COUNT * nr + FV_COUNT * nv + FY_COUNT * ny;
-}
+// FAST-mode factor tables per problem (host-built, lowering.cpp), array-of-
+// structs per node index so one base address serves every field. They hold the
+// separable pieces of g1..g6 (discretization.cpp:56-72) with the stencil 1/dx
+// factors folded in, plus the v-line LU, which depends on j only:
+//   g1/dxr^2 = G1[i] v_j      g4/(2dxr) = c4 G4C[i] + G4P[i] + G4Q[i] y_k + G4V[i] v_j
+//   g3/(4 dxr dxv) = G3[i] G3V[j]     g2/dxv^2 = G2[j]     g5/(2dxv) = G5[j]
+//   g6/(2dxy) = A[i] v_j S6[k] + T6[k]                   reaction = REACT[i]
+// v-line LU: dp_j = RP_j x_j + B_j dp_{j-1} (B = -RP L), x_j = dp_j + E_j x_{j+1}
+// (E = -CP), with in-segment products BF/BB for the segmented v-solve.
+constexpr int kFR = 8;
+enum FastR : int { FR_G1 = 0, FR_G4C, FR_G4P, FR_G4Q, FR_G4V, FR_G3, FR_REACT, FR_A };
+constexpr int kFV = 10;
+enum FastV : int { FV_V = 0, FV_G2, FV_G5, FV_G3, FV_B, FV_E, FV_RP, FV_BF, FV_BB, FV_PAD };
+constexpr int kFY = 4;
+enum FastY : int { FY_S6 = 0, FY_T6, FY_Y, FY_PAD };
+constexpr int kSegV = 16;  // rows per segment of the segmented v-solve
+inline int fast_table_stride(int nr, int nv, int ny) { return kFR * nr + kFV * nv + kFY * ny; }
 
 // Per-kernel hook for the live profiler: called after each launch with the
 // kernel's index, name and ALGORITHMIC bytes per grid point of that launch.

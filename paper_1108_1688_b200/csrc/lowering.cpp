@@ -355,8 +355,8 @@ std::vector<double> build_fast_tables(const Lowered& L, const hjmsv_solver_confi
     const int nr = L.nr, nv = L.nv, ny = L.ny;
     std::vector<double> t(fast_table_stride(nr, nv, ny), 0.0);
     double* R = t.data();
-    double* V = R + FR_COUNT * nr;
-    double* Y = V + FV_COUNT * nv;
+    double* V = R + kFR * nr;
+    double* Y = V + kFV * nv;
     const double dxr = L.r.dx(), dxv = L.v.dx(), dxy = L.y.dx();
     const double inv_dxr2 = nr > 1 ? 1.0 / (dxr * dxr) : 0.0;
     const double inv_2dxr = nr > 1 ? 0.5 / dxr : 0.0;
@@ -369,37 +369,40 @@ std::vector<double> build_fast_tables(const Lowered& L, const hjmsv_solver_confi
     const double* b = a + nr;
     for (int i = 0; i < nr; ++i) {
         const double jr = L.r.j1[i];
-        R[FR_G1 * nr + i] = a[i] / (jr * jr) * inv_dxr2;
-        R[FR_G4C * nr + i] = inv_2dxr / jr;
-        R[FR_G4P * nr + i] = -pc.kappa * L.r.z[i] / jr * inv_2dxr;
-        R[FR_G4Q * nr + i] = pc.r0 / jr * inv_2dxr;
-        R[FR_G4V * nr + i] = -a[i] * L.r.j2[i] / (jr * jr * jr) * inv_2dxr;
-        R[FR_G3 * nr + i] = b[i] / jr * inv_cross;
-        R[FR_REACT * nr + i] = L.r.z[i] * pc.r0;
-        R[FR_A * nr + i] = a[i];
+        double* e = R + kFR * i;
+        e[FR_G1] = a[i] / (jr * jr) * inv_dxr2;
+        e[FR_G4C] = inv_2dxr / jr;
+        e[FR_G4P] = -pc.kappa * L.r.z[i] / jr * inv_2dxr;
+        e[FR_G4Q] = pc.r0 / jr * inv_2dxr;
+        e[FR_G4V] = -a[i] * L.r.j2[i] / (jr * jr * jr) * inv_2dxr;
+        e[FR_G3] = b[i] / jr * inv_cross;
+        e[FR_REACT] = L.r.z[i] * pc.r0;
+        e[FR_A] = a[i];
     }
     for (int j = 0; j < nv; ++j) {
         const double v = L.v.z[j], jv = L.v.j1[j];
-        V[FV_V * nv + j] = v;
-        V[FV_G2 * nv + j] = pc.half_eps2 * v / (jv * jv) * inv_dxv2;
-        V[FV_G5 * nv + j] =
-            (pc.theta * (1.0 - v) / jv - pc.half_eps2 * v * L.v.j2[j] / (jv * jv * jv)) * inv_2dxv;
-        V[FV_G3 * nv + j] = v / jv;
+        double* e = V + kFV * j;
+        e[FV_V] = v;
+        e[FV_G2] = pc.half_eps2 * v / (jv * jv) * inv_dxv2;
+        e[FV_G5] = (pc.theta * (1.0 - v) / jv - pc.half_eps2 * v * L.v.j2[j] / (jv * jv * jv)) *
+                   inv_2dxv;
+        e[FV_G3] = v / jv;
     }
     // v-line LU (rows of assemble_line_v, discretization.cpp:232-259, depend on j only)
     if (nv > 1) {
         double cp_prev = 0.0;
         for (int j = 0; j < nv; ++j) {
+            double* e = V + kFV * j;
             double l = 0.0, d = 1.0, u = 0.0;
             const bool dir = (j == 0 && pc.rule[F_VMIN] == RULE_DIRICHLET) ||
                              (j == nv - 1 && pc.rule[F_VMAX] == RULE_DIRICHLET);
             if (!dir) {
-                const double g5h = V[FV_G5 * nv + j];
+                const double g5h = e[FV_G5];
                 if (j == 0) {
                     d = 1.0 + th * 2.0 * g5h;
                     u = -th * 2.0 * g5h;
                 } else {
-                    const double w2 = th * V[FV_G2 * nv + j], w1 = th * g5h;
+                    const double w2 = th * e[FV_G2], w1 = th * g5h;
                     l = w1 - w2;
                     d = 1.0 + 2.0 * w2;
                     u = -(w2 + w1);
@@ -408,15 +411,31 @@ std::vector<double> build_fast_tables(const Lowered& L, const hjmsv_solver_confi
             const double piv = j == 0 ? d : d - l * cp_prev;
             const double rp = std::abs(piv) < 1e-300 ? std::nan("") : 1.0 / piv;
             cp_prev = u * rp;
-            V[FV_L * nv + j] = l;
-            V[FV_CP * nv + j] = cp_prev;
-            V[FV_RP * nv + j] = rp;
+            e[FV_B] = -rp * l;
+            e[FV_E] = -cp_prev;
+            e[FV_RP] = rp;
+        }
+        // in-segment products for the segmented solve
+        for (int s0 = 0; s0 < nv; s0 += kSegV) {
+            const int s1 = std::min(nv, s0 + kSegV) - 1;
+            double pf = 1.0;
+            for (int j = s0; j <= s1; ++j) {
+                pf *= V[kFV * j + FV_B];
+                V[kFV * j + FV_BF] = pf;
+            }
+            double pb = 1.0;
+            for (int j = s1; j >= s0; --j) {
+                pb *= V[kFV * j + FV_E];
+                V[kFV * j + FV_BB] = pb;
+            }
         }
     }
     for (int k = 0; k < ny; ++k) {
         const double jy = L.y.j1[k];
-        Y[FY_S6 * ny + k] = 2.0 * inv_2dxy / jy;
-        Y[FY_T6 * ny + k] = -2.0 * pc.kappa * L.y.z[k] / jy * inv_2dxy;
+        double* e = Y + kFY * k;
+        e[FY_S6] = 2.0 * inv_2dxy / jy;
+        e[FY_T6] = -2.0 * pc.kappa * L.y.z[k] / jy * inv_2dxy;
+        e[FY_Y] = L.y.z[k];
     }
     (void)cfg;
     return t;
