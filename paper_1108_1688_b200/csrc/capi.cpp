@@ -94,7 +94,7 @@ struct hjmsv_solver {
     std::vector<double> bound;
     // device
     double *U = nullptr, *D = nullptr, *C = nullptr, *U0 = nullptr;
-    double *axes = nullptr, *steps = nullptr, *fast = nullptr;
+    double *axes = nullptr, *steps = nullptr, *fast = nullptr, *fb = nullptr;
     ProblemConst* pc = nullptr;
     DevStatus* st = nullptr;
     long long* spot_idx = nullptr;
@@ -115,7 +115,7 @@ struct hjmsv_solver {
         if (device >= 0) cudaSetDevice(device);
         if (graph) cudaGraphExecDestroy(graph);
         for (void* p : {(void*)U, (void*)D, (void*)C, (void*)U0, (void*)axes, (void*)steps,
-                        (void*)fast, (void*)pc, (void*)st, (void*)spot_idx, (void*)spot_w,
+                        (void*)fast, (void*)fb, (void*)pc, (void*)st, (void*)spot_idx, (void*)spot_w,
                         (void*)spot_out})
             dfree(p);
         if (ev0) cudaEventDestroy(ev0);
@@ -309,6 +309,9 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         v.fast_stride = fast_stride(h->nr, h->nv, h->ny);
         h->fast = dalloc<double>(static_cast<size_t>(count) * v.fast_stride);
         v.fast = h->fast;
+        v.fb_stride = 2 * h->ny + 2 * h->nr + 2 * h->nr * h->ny;
+        h->fb = dalloc<double>(static_cast<size_t>(count) * v.fb_stride);
+        v.fb = h->fb;
         for (int p = 0; p < count; ++p) {
             const std::vector<double> ft = build_fast_tables(L[p], cfg, L[p].pc.theta_dt);
             CK(cudaMemcpy(h->fast + static_cast<size_t>(p) * v.fast_stride, ft.data(),

@@ -67,6 +67,8 @@ struct BatchView {
     int fast_stride;
     int apply_only;       // stage mode: D = F(U), Dirichlet nodes 0 (apply_operator)
     int dmask;            // bit f set when face f is Dirichlet (uniform across the batch)
+    double* fb;           // [P][fb_stride] Dirichlet face values at t_next of the current step
+    int fb_stride;        // 2ny (r faces) + 2nr (y faces) + 2 nr ny (v faces)
 };
 
 inline int axes_stride(int nr, int nv, int ny) { return 5 * nr + 3 * nv + 3 * ny; }

@@ -28,6 +28,7 @@
 // reduced pivots stand in for the global ones in the singular-pivot check.
 // Parity with the reference is 1e-10 normwise (tests/test_gpu_parity.py).
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels_common.cuh"
 
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(512) k_fx_r(BatchView v, int s) {
 // are affine scans: a block of 32 k x S segments (kSegV rows) computes local
 // scans, carries the segment boundary values across segments in shared memory,
 // and fixes its rows up with the in-segment products BF/BB.
-__global__ void __launch_bounds__(512) k_fx_v(BatchView v, int s) {
+__global__ void __launch_bounds__(512, 2) k_fx_v(BatchView v, int s) {
     extern __shared__ double car[];  // [2][S][32]
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
@@ -646,7 +647,451 @@ void launch_y(const BatchView& v, int s, cudaStream_t stream) {
     k_fx_y<LY><<<dim3((lines + lpb - 1) / lpb, v.P), 256, 0, stream>>>(v, s);
 }
 
+// ============================================================ face values
+// Dirichlet values at t_next for the current step, one table per face, filled
+// once per step (k_faces) so the hot kernels never evaluate exp():
+//   r faces [ny] (at i = nr-1 / 0), y faces [nr] (at k = ny-1 / 0), v faces [nr][ny].
+__device__ __forceinline__ int fb_offset(const BatchView& v, int face, int i, int k) {
+    const int ny = v.ny, nr = v.nr;
+    switch (face) {
+        case F_RMAX: return k;
+        case F_RMIN: return ny + k;
+        case F_YMAX: return 2 * ny + i;
+        case F_YMIN: return 2 * ny + nr + i;
+        case F_VMAX: return 2 * ny + 2 * nr + i * ny + k;
+        default: return 2 * ny + 2 * nr + nr * ny + i * ny + k;
+    }
+}
+
+__device__ __forceinline__ double fval(const BatchView& v, int p, int face, int i, int k) {
+    return __ldg(v.fb + static_cast<size_t>(p) * v.fb_stride + fb_offset(v, face, i, k));
+}
+
+__global__ void __launch_bounds__(256) k_faces(BatchView v, int s) {
+    const int p = blockIdx.y;
+    if (v.st[p].fail_step) return;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= v.fb_stride) return;
+    const int nr = v.nr, ny = v.ny;
+    int face, i, k;
+    if (q < ny) {
+        face = F_RMAX; i = nr - 1; k = q;
+    } else if (q < 2 * ny) {
+        face = F_RMIN; i = 0; k = q - ny;
+    } else if (q < 2 * ny + nr) {
+        face = F_YMAX; i = q - 2 * ny; k = ny - 1;
+    } else if (q < 2 * ny + 2 * nr) {
+        face = F_YMIN; i = q - 2 * ny - nr; k = 0;
+    } else {
+        int t = q - 2 * ny - 2 * nr;
+        face = t < nr * ny ? F_VMAX : F_VMIN;
+        if (t >= nr * ny) t -= nr * ny;
+        i = t / ny;
+        k = t - i * ny;
+    }
+    double val = 0.0;
+    if (v.dmask >> face & 1)
+        val = face_value(v.pc[p], step_row(v, p, s), tables(v, p), face, i, k);
+    v.fb[static_cast<size_t>(p) * v.fb_stride + q] = val;
+}
+
+// out-of-line slow paths (take the view by value so the kernels' own copy stays
+// in the parameter bank and their loads stay LDG)
+__device__ __noinline__ void guard_fail(const BatchView v, int p, int s, unsigned long long flat,
+                                        double un) {
+    DevStatus& st = v.st[p];
+    if (!isfinite(un)) {  // guard_finite (solver.cpp:69-77)
+        atomicMin(&st.nonfinite_first, flat);
+        mark_fail(st, s + 1, HJMSV_NONFINITE);
+    } else {
+        atomicMin(&st.diverge_first, flat);
+        mark_fail(st, s + 1, HJMSV_DIVERGED);
+    }
+}
+
+// dU0 at a node of a face plane i, a face row j (generic stencil, one-sided rows)
+__device__ __noinline__ double explicit_slow(const BatchView v, int p, int s, int i, int j,
+                                             int k) {
+    const int nr = v.nr, nv = v.nv, ny = v.ny;
+    const ProblemConst& pc = v.pc[p];
+    const double* step = step_row(v, p, s);
+    const int sr = nv * ny;
+    const double* u = v.U + static_cast<size_t>(p) * v.N + (static_cast<size_t>(i) * nv + j) * ny + k;
+    const int face = dface(v, i, j, k);
+    if (face >= 0) return v.apply_only ? 0.0 : fval(v, p, face, i, k) - u[0];
+    const FT F = ftab(v, p);
+    const double* R = F.R + kFR * i;
+    const double* V = F.V + kFV * j;
+    const double* Y = F.Y + kFY * k;
+    const double vj = V[FV_V];
+    const double g1s = R[FR_G1] * vj;
+    const double g4h =
+        fma(step[ST_C4], R[FR_G4C], fma(R[FR_G4Q], Y[FY_Y], fma(R[FR_G4V], vj, R[FR_G4P])));
+    const double g6h = fma(R[FR_A] * vj, Y[FY_S6], Y[FY_T6]);
+    const double u0 = u[0];
+    double acc = -R[FR_REACT] * u0;
+    if (i == 0) {
+        const double u1 = u[sr];
+        if (v.r_order == 1)
+            acc = fma(2.0 * g4h, u1 - u0, acc);
+        else
+            acc = fma(g4h, fma(4.0, u1, -u[2 * sr]) - 3.0 * u0, acc);
+    } else {
+        const double up = u[sr], dn = u[-sr];
+        acc = fma(g1s, (up + dn) - 2.0 * u0, acc);
+        acc = fma(g4h, up - dn, acc);
+    }
+    if (j == 0) {
+        acc = fma(2.0 * V[FV_G5], u[ny] - u0, acc);
+    } else {
+        const double up = u[ny], dn = u[-ny];
+        acc = fma(V[FV_G2], (up + dn) - 2.0 * u0, acc);
+        acc = fma(V[FV_G5], up - dn, acc);
+    }
+    if (k == 0) {
+        const double u1 = u[1];
+        if (v.y_order == 1)
+            acc = fma(2.0 * g6h, u1 - u0, acc);
+        else
+            acc = fma(g6h, fma(4.0, u1, -u[2]) - 3.0 * u0, acc);
+    } else {
+        acc = fma(g6h, u[1] - u[-1], acc);
+    }
+    if (i > 0 && i < nr - 1 && j > 0 && j < nv - 1)
+        acc = fma(R[FR_G3] * V[FV_G3], (u[sr + ny] - u[sr - ny]) - (u[ny - sr] - u[-sr - ny]), acc);
+    return acc * pc.dt;
+}
+
+// ============================================================ shape-specialised
+// Instantiated for compile-time (NV, NY) so strides are immediate offsets;
+// fast_step dispatches to them for the benchmark shapes and falls back to the
+// runtime-shape kernels above otherwise.
+
+// ------------------------------------------------------------ explicit, 2.5D
+// Block = 32 k x 8 j; each thread marches TI planes of its column (fully
+// unrolled) with a register window of U(i-1..i+1, j-1..j+1, k); k+-1 arrive by
+// shuffles. Loads use clamped indices (no branches); the y faces and the
+// one-sided y row are selects; face planes (i = 0, nr-1) and face rows
+// (j = 0, nv-1) take the out-of-line generic path, uniformly per warp.
+template <int NV, int NY, int TI, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_ex3(BatchView v, int s) {
+    __shared__ double rt[TI][kFR];
+    const int p = blockIdx.z;
+    DevStatus& st = v.st[p];
+    if (st.fail_step) return;
+    const int nr = v.nr;
+    const int i0 = blockIdx.y * TI;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) st.maxdelta_bits = 0ull;
+    const FT F = ftab(v, p);
+    if (tid < TI * kFR) {
+        const int ii = min(i0 + tid / kFR, nr - 1);
+        rt[tid / kFR][tid % kFR] = F.R[kFR * ii + tid % kFR];
+    }
+    constexpr int TK = NY / 32 > 0 ? NY / 32 : 1;
+    constexpr int SR = NV * NY;
+    const int jt = blockIdx.x / TK;
+    const int k = (blockIdx.x - jt * TK) * 32 + threadIdx.x;
+    const int j = jt * 8 + threadIdx.y;
+    const size_t off = static_cast<size_t>(p) * v.N;
+    __syncthreads();
+    if (j == 0 || j == NV - 1) {  // face rows: generic path (whole warp)
+#pragma unroll 1
+        for (int t = 0; t < TI; ++t) {
+            const int i = i0 + t;
+            if (i < nr)
+                v.D[off + (static_cast<size_t>(i) * NV + j) * NY + k] = explicit_slow(v, p, s, i, j, k);
+        }
+        return;
+    }
+    const double* __restrict__ col = v.U + off + j * NY + k;
+    double* __restrict__ dcol = v.D + off + j * NY + k;
+    const double* Vt = F.V + kFV * j;
+    const double* Yt = F.Y + kFY * k;
+    const double vj = Vt[FV_V], g2s = Vt[FV_G2], g5h = Vt[FV_G5], g3v = Vt[FV_G3];
+    const double yk = Yt[FY_Y], vs6 = vj * Yt[FY_S6], t6 = Yt[FY_T6];
+    const double dtm = v.pc[p].dt;
+    const double c4 = step_row(v, p, s)[ST_C4];
+    const bool k0 = k == 0, kN = k == NY - 1;
+    const bool ymaxF = kN && dir(v, F_YMAX) && !v.apply_only;
+    const bool yminF = k0 && dir(v, F_YMIN) && !v.apply_only;
+    const bool zeroF = (kN && dir(v, F_YMAX)) || (k0 && dir(v, F_YMIN));
+    const bool order2y = v.y_order != 1;
+    const double* fby = v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY + (kN ? 0 : nr);
+    auto load = [&](int ii, double& m, double& c, double& pl) {
+        const double* q = col + static_cast<size_t>(min(max(ii, 0), nr - 1)) * SR;
+        c = __ldg(q);
+        m = __ldg(q - NY);
+        pl = __ldg(q + NY);
+    };
+    double wm0, wm1, wm2, w00, w01, w02;
+    load(i0 - 1, wm0, wm1, wm2);
+    load(i0, w00, w01, w02);
+#pragma unroll
+    for (int t = 0; t < TI; ++t) {
+        const int i = i0 + t;
+        double wp0, wp1, wp2;
+        load(i + 1, wp0, wp1, wp2);
+        double kl = __shfl_up_sync(0xffffffffu, w01, 1);
+        double kr = __shfl_down_sync(0xffffffffu, w01, 1);
+        const double* q = col + static_cast<size_t>(min(i, nr - 1)) * SR;
+        if (threadIdx.x == 0 && !k0) kl = __ldg(q - 1);
+        if (threadIdx.x == 31 && !kN) kr = __ldg(q + 1);
+        const double k2 = k0 ? __ldg(q + 2) : 0.0;
+        const double fbv = (ymaxF || yminF) ? __ldg(fby + min(i, nr - 1)) : 0.0;
+        if (i < nr) {
+            double out;
+            if (i > 0 && i < nr - 1) {
+                const double* R = rt[t];
+                const double g4h = fma(c4, R[FR_G4C], fma(R[FR_G4Q], yk, fma(R[FR_G4V], vj, R[FR_G4P])));
+                const double u0 = w01;
+                double acc = -R[FR_REACT] * u0;
+                acc = fma(R[FR_G1] * vj, (wp1 + wm1) - 2.0 * u0, acc);
+                acc = fma(g4h, wp1 - wm1, acc);
+                acc = fma(g2s, (w02 + w00) - 2.0 * u0, acc);
+                acc = fma(g5h, w02 - w00, acc);
+                acc = fma(R[FR_G3] * g3v, (wp2 - wp0) - (wm2 - wm0), acc);
+                // one-sided y row at k = 0 (discretization.cpp:346-352)
+                const double yd = k0 ? (order2y ? fma(4.0, kr, -k2) - 3.0 * u0 : 2.0 * (kr - u0))
+                                     : kr - kl;
+                acc = fma(fma(R[FR_A], vs6, t6), yd, acc);
+                out = acc * dtm;
+                out = zeroF ? ((ymaxF || yminF) ? fbv - u0 : 0.0) : out;
+            } else {
+                out = explicit_slow(v, p, s, i, j, k);
+            }
+            dcol[static_cast<size_t>(i) * SR] = out;
+        }
+        wm0 = w00; wm1 = w01; wm2 = w02;
+        w00 = wp0; w01 = wp1; w02 = wp2;
+    }
+}
+
+// ------------------------------------------------------------ explicit, per node
+// Thread per node, block = 32 k x 8 j of one plane: latency is hidden by
+// occupancy (every load is independent), neighbours come from L1. Face planes
+// and face rows (uniform per block / warp) take the generic out-of-line path;
+// k edges are selects.
+template <int NV, int NY>
+__global__ void __launch_bounds__(256) k_ex4(BatchView v, int s) {
+    const int p = blockIdx.z, i = blockIdx.y;
+    DevStatus& st = v.st[p];
+    if (st.fail_step) return;
+    constexpr int TK = NY / 32 > 0 ? NY / 32 : 1;
+    constexpr int SR = NV * NY;
+    const int jt = blockIdx.x / TK;
+    const int k = (blockIdx.x - jt * TK) * 32 + threadIdx.x;
+    const int j = jt * 8 + threadIdx.y;
+    if (blockIdx.x == 0 && i == 0 && threadIdx.x == 0 && threadIdx.y == 0) st.maxdelta_bits = 0ull;
+    const int nr = v.nr;
+    const size_t off = static_cast<size_t>(p) * v.N;
+    const int q = (i * NV + j) * NY + k;
+    if (i == 0 || i == nr - 1 || j == 0 || j == NV - 1) {
+        v.D[off + q] = explicit_slow(v, p, s, i, j, k);
+        return;
+    }
+    const double* __restrict__ u = v.U + off + q;
+    const double u0 = __ldg(u);
+    double kl = __shfl_up_sync(0xffffffffu, u0, 1);
+    double kr = __shfl_down_sync(0xffffffffu, u0, 1);
+    const bool k0 = k == 0, kN = k == NY - 1;
+    if (threadIdx.x == 0 && !k0) kl = __ldg(u - 1);
+    if (threadIdx.x == 31 && !kN) kr = __ldg(u + 1);
+    const double rp = __ldg(u + SR), rm = __ldg(u - SR);
+    const double vp = __ldg(u + NY), vm = __ldg(u - NY);
+    const double cross = (__ldg(u + SR + NY) - __ldg(u + SR - NY)) - (__ldg(u - SR + NY) - __ldg(u - SR - NY));
+    const FT F = ftab(v, p);
+    const double2* R2 = reinterpret_cast<const double2*>(F.R + kFR * i);
+    const double2 r01 = __ldg(R2), r23 = __ldg(R2 + 1), r45 = __ldg(R2 + 2), r67 = __ldg(R2 + 3);
+    // r01 = (G1, G4C), r23 = (G4P, G4Q), r45 = (G4V, G3), r67 = (REACT, A)
+    const double2* V2 = reinterpret_cast<const double2*>(F.V + kFV * j);
+    const double2 v01 = __ldg(V2), v23 = __ldg(V2 + 1);  // (V, G2), (G5, G3V)
+    const double2* Y2 = reinterpret_cast<const double2*>(F.Y + kFY * k);
+    const double2 y01 = __ldg(Y2), y23 = __ldg(Y2 + 1);  // (S6, T6), (Y, pad)
+    const double vj = v01.x;
+    const double c4 = __ldg(step_row(v, p, s) + ST_C4);
+    const double g4h = fma(c4, r01.y, fma(r23.y, y23.x, fma(r45.x, vj, r23.x)));
+    const double g6h = fma(r67.y * vj, y01.x, y01.y);
+    double acc = -r67.x * u0;
+    acc = fma(r01.x * vj, (rp + rm) - 2.0 * u0, acc);
+    acc = fma(g4h, rp - rm, acc);
+    acc = fma(v01.y, (vp + vm) - 2.0 * u0, acc);
+    acc = fma(v23.x, vp - vm, acc);
+    acc = fma(r45.y * v23.y, cross, acc);
+    double yd = kr - kl;
+    if (k0) {  // one-sided y row (discretization.cpp:346-352)
+        const double k2 = __ldg(u + 2);
+        yd = v.y_order != 1 ? fma(4.0, kr, -k2) - 3.0 * u0 : 2.0 * (kr - u0);
+    }
+    acc = fma(g6h, yd, acc);
+    double out = acc * v.pc[p].dt;
+    if ((kN && dir(v, F_YMAX)) || (k0 && dir(v, F_YMIN)))
+        out = v.apply_only ? 0.0 : fval(v, p, kN ? F_YMAX : F_YMIN, i, k) - u0;
+    v.D[off + q] = out;
+}
+
+// ------------------------------------------------------------ y-lines + update
+// NY/MY lanes per line (MY contiguous rows per lane, 128-bit loads/stores).
+template <int NV, int NY, int MY>
+__global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
+    constexpr int kSegY = MY;
+    constexpr int LY = NY / kSegY;
+    constexpr int LPW = 32 / LY;
+    __shared__ double rs[8][32][8];
+    const int p = blockIdx.y;
+    DevStatus& st = v.st[p];
+    if (st.fail_step) return;
+    const int nr = v.nr;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int sy = lane % LY;
+    const int base = lane - sy;
+    const int line = (blockIdx.x * 8 + wid) * LPW + lane / LY;
+    const bool live = line < nr * NV;
+    const int lc = live ? line : 0;
+    const int i = lc / NV, j = lc - (lc / NV) * NV;
+    const size_t off = static_cast<size_t>(p) * v.N;
+    const size_t lb = off + static_cast<size_t>(lc) * NY + sy * kSegY;
+    double x[kSegY], cs[kSegY], al[kSegY];
+    {
+        const double2* d2 = reinterpret_cast<const double2*>(v.D + lb);
+#pragma unroll
+        for (int q = 0; q < kSegY / 2; ++q) {
+            const double2 t = __ldg(d2 + q);
+            x[2 * q] = t.x;
+            x[2 * q + 1] = t.y;
+        }
+    }
+    const bool dI = (i == nr - 1 && dir(v, F_RMAX)) || (i == 0 && dir(v, F_RMIN));
+    const bool dJ = (j == NV - 1 && dir(v, F_VMAX)) || (j == 0 && dir(v, F_VMIN));
+    const bool solve = live && !dI && !dJ;  // !is_dirichlet(i,j,1) (solver.cpp:156)
+    const bool yminD = dir(v, F_YMIN), ymaxD = dir(v, F_YMAX);
+    double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
+    if (solve) {
+        const ProblemConst& pc = v.pc[p];
+        const FT F = ftab(v, p);
+        const double th = pc.theta_dt;
+        const double h1 = F.R[kFR * i + FR_A] * F.V[kFV * j + FV_V];
+        const double react = F.R[kFR * i + FR_REACT];
+        const double dint = fma(th, react, 1.0);
+        double lr[kSegY];
+        double g60 = 0.0;
+#pragma unroll
+        for (int r = 0; r < kSegY; ++r) {
+            const double2 st6 = __ldg(reinterpret_cast<const double2*>(F.Y + kFY * (sy * kSegY + r)));
+            const double g6h = fma(h1, st6.x, st6.y);
+            if (r == 0) g60 = g6h;
+            lr[r] = th * g6h;
+        }
+        double f0d = dint, f0u = -lr[0];
+        if (sy == 0) {  // row 0 of the line (discretization.cpp:274-289), folded (solver.cpp:28-40)
+            f0d = 1.0;
+            f0u = 0.0;
+            if (!yminD) {
+                if (v.y_order == 1) {
+                    f0d = fma(th, fma(2.0, g60, react), 1.0);
+                    f0u = -2.0 * lr[0];
+                } else {
+                    f0d = fma(th, fma(3.0, g60, react), 1.0);
+                    f0u = -4.0 * lr[0];
+                    const double s20 = lr[0];
+                    const double l1 = lr[1], u1 = -lr[1];
+                    if (fabs(u1) > 1e-300) {
+                        const double f = s20 / u1;
+                        f0d = fma(-f, l1, f0d);
+                        f0u = fma(-f, dint, f0u);
+                        x[0] = fma(-f, x[1], x[0]);
+                    } else {
+                        x[0] = fma(-s20, x[2], x[0]);
+                    }
+                }
+            }
+        }
+        const bool lastI = sy == LY - 1 && ymaxD;
+        auto row = [&](int r, double& l, double& d, double& u) {
+            if (r == 0 && sy == 0) {
+                l = 0.0;
+                d = f0d;
+                u = f0u;
+            } else if (r == kSegY - 1 && lastI) {
+                l = 0.0;
+                d = 1.0;
+                u = 0.0;
+            } else {
+                l = lr[r];
+                d = dint;
+                u = -lr[r];
+            }
+        };
+        int bad_r = 0;
+        if (!seg_solve<kSegY>(kSegY, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row))
+            record_pivot(st, s, 2, line, sy * kSegY + bad_r);
+    }
+    double left = 0.0, right = 0.0;
+    if (LY > 1) {
+        double* E = &rs[wid][base][0];
+        double* e = E + sy * 8;
+        e[0] = yF; e[1] = aF; e[2] = bF; e[3] = yL; e[4] = aL; e[5] = bL;
+        __syncwarp();
+        if (sy == 0 && solve) {
+            int bt = 0;
+            if (!reduced_solve(E, LY, 8, bt)) record_pivot(st, s, 2, line, bt * kSegY);
+        }
+        __syncwarp();
+        left = sy > 0 ? E[(sy - 1) * 8 + 6] : 0.0;
+        right = sy < LY - 1 ? e[7] : 0.0;
+    }
+    // x_r, then U += dU, Dirichlet values, max|dU|, guard (solver.cpp:163-176)
+    double md = 0.0;
+    if (live) {
+        double2* u2 = reinterpret_cast<double2*>(v.U + lb);
+        double un[kSegY];
+#pragma unroll
+        for (int q = 0; q < kSegY / 2; ++q) {
+            const double2 t = u2[q];
+            un[2 * q] = t.x;
+            un[2 * q + 1] = t.y;
+        }
+        double b = bL;
+#pragma unroll
+        for (int r = kSegY - 1; r >= 0; --r) {
+            double dq = x[r];
+            if (solve) {
+                if (r < kSegY - 1) b = -cs[r] * b;
+                dq = fma(b, right, fma(al[r], left, x[r]));
+            }
+            un[r] += dq;
+            md = fmax(md, fabs(dq));
+        }
+        if (!solve) {
+#pragma unroll
+            for (int r = 0; r < kSegY; ++r) {
+                const int kk = sy * kSegY + r;
+                un[r] = fval(v, p, dface(v, i, j, kk), i, kk);
+            }
+        } else {
+            const double* fby = v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY;
+            if (sy == 0 && yminD) un[0] = __ldg(fby + nr + i);
+            if (sy == LY - 1 && ymaxD) un[kSegY - 1] = __ldg(fby + i);
+        }
+        const double bound = v.pc[p].bound;
+#pragma unroll
+        for (int r = 0; r < kSegY; ++r)
+            if (!(fabs(un[r]) <= bound)) guard_fail(v, p, s, lb - off + r, un[r]);
+#pragma unroll
+        for (int q = 0; q < kSegY / 2; ++q) u2[q] = make_double2(un[2 * q], un[2 * q + 1]);
+    }
+    for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+    if (lane == 0 && md > 0.0)
+        atomicMax(&st.maxdelta_bits, static_cast<unsigned long long>(__double_as_longlong(md)));
+}
+
 }  // namespace
+
+// (nv, ny) pairs with compile-time kernels: nv == ny in {32, 64, 128, 256}
+int specialised_shape(const BatchView& v) {
+    if (v.nv != v.ny) return 0;
+    return (v.ny == 32 || v.ny == 64 || v.ny == 128 || v.ny == 256) ? v.ny : 0;
+}
 
 bool fast_supported(int nr, int nv, int ny) {
     // collapsed axes are served by STRICT; segment counts bounded by the block shapes
@@ -667,7 +1112,30 @@ void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launch
     // algorithmic bytes per node of each launch (SURVEY §8d accounting): read U,
     // write dU0 | read + write the line | read + write the line | read dU, read U, write U
     const int tk = (v.ny + 31) / 32, tj = (v.nv + 7) / 8;
-    k_fx_explicit<<<dim3(tk * tj, v.nr, v.P), dim3(32, 8), 0, stream>>>(v, s);
+    const int shape = specialised_shape(v);
+    k_faces<<<dim3((v.fb_stride + 255) / 256, v.P), 256, 0, stream>>>(v, s);
+    mark(4, "fx_faces", 0.0);
+    constexpr int TI = 8;
+    const dim3 gex(tk * tj, (v.nr + TI - 1) / TI, v.P);
+    static const int exv = [] {
+        const char* e = std::getenv("HJMSV_EX_MINB");
+        return e ? std::atoi(e) : 0;
+    }();
+#define HJ_EX(NVV, MB) k_ex3<NVV, NVV, TI, MB><<<gex, dim3(32, 8), 0, stream>>>(v, s)
+#define HJ_EXS(NVV)                   \
+    if (exv == 0) k_ex4<NVV, NVV><<<dim3(tk * tj, v.nr, v.P), dim3(32, 8), 0, stream>>>(v, s); \
+    else if (exv >= 4) HJ_EX(NVV, 4);       \
+    else if (exv == 3) HJ_EX(NVV, 3);  \
+    else HJ_EX(NVV, 2)
+    switch (shape) {
+        case 32: HJ_EXS(32); break;
+        case 64: HJ_EXS(64); break;
+        case 128: HJ_EXS(128); break;
+        case 256: HJ_EXS(256); break;
+        default: k_fx_explicit<<<dim3(tk * tj, v.nr, v.P), dim3(32, 8), 0, stream>>>(v, s);
+    }
+#undef HJ_EXS
+#undef HJ_EX
     mark(0, "fx_explicit", 16.0);
     const int Sr = (v.nr + kSegR - 1) / kSegR;
     const int tkr = (v.ny + kLanesR - 1) / kLanesR;
@@ -678,7 +1146,24 @@ void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launch
     k_fx_v<<<dim3(v.nr * tk, v.P), dim3(32, Sv), 2ull * Sv * 32 * sizeof(double), stream>>>(v, s);
     mark(2, "fx_sweep_v", 16.0);
     const int ly = (v.ny + kSegY - 1) / kSegY;
-    if (ly <= 1)
+    const int lines = v.nr * v.nv;
+    static const int ymy = [] {
+        const char* e = std::getenv("HJMSV_Y_ROWS");
+        return e ? std::atoi(e) : 16;
+    }();
+    if (shape == 32) {
+        if (ymy == 8) k_y3<32, 32, 8><<<dim3((lines + 63) / 64, v.P), 256, 0, stream>>>(v, s);
+        else k_y3<32, 32, 16><<<dim3((lines + 127) / 128, v.P), 256, 0, stream>>>(v, s);
+    } else if (shape == 64) {
+        if (ymy == 8) k_y3<64, 64, 8><<<dim3((lines + 31) / 32, v.P), 256, 0, stream>>>(v, s);
+        else k_y3<64, 64, 16><<<dim3((lines + 63) / 64, v.P), 256, 0, stream>>>(v, s);
+    } else if (shape == 128) {
+        if (ymy == 8) k_y3<128, 128, 8><<<dim3((lines + 15) / 16, v.P), 256, 0, stream>>>(v, s);
+        else k_y3<128, 128, 16><<<dim3((lines + 31) / 32, v.P), 256, 0, stream>>>(v, s);
+    } else if (shape == 256) {
+        if (ymy == 8) k_y3<256, 256, 8><<<dim3((lines + 7) / 8, v.P), 256, 0, stream>>>(v, s);
+        else k_y3<256, 256, 16><<<dim3((lines + 15) / 16, v.P), 256, 0, stream>>>(v, s);
+    } else if (ly <= 1)
         launch_y<1>(v, s, stream);
     else if (ly <= 2)
         launch_y<2>(v, s, stream);
