@@ -181,6 +181,8 @@ class Solver:
         out = []
         for q in range(nk.value):
             nm = names.raw[q * L:(q + 1) * L].split(b"\0", 1)[0].decode()
+            if not nm:  # index slot unused by this step variant
+                continue
             out.append({"name": nm, "avg_ms": float(ms[q]), "alg_bytes": float(by[q])})
         return out, n.value
 

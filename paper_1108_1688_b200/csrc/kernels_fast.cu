@@ -30,10 +30,13 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "kernels_common.cuh"
 
 namespace hjmsv_b200 {
 namespace {
+namespace cg = cooperative_groups;
 using namespace dev;
 
 constexpr int kSegR = 16;  // rows per r-segment
@@ -1085,6 +1088,640 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
         atomicMax(&st.maxdelta_bits, static_cast<unsigned long long>(__double_as_longlong(md)));
 }
 
+// ------------------------------------------------------------ pass A, fused
+// Explicit operator + r-lines in one kernel. Block = 16 consecutive k (same j)
+// x S segments of 16 rows i; each thread marches its segment with a register
+// window of U at (i-1..i+1) x (j-1..j+1) fed by a per-thread cp.async ring
+// (kRing rows ahead), k+-1 by shuffles inside the 16-lane group. It computes
+// dU0 = dt F(U) (apply_operator, discretization.cpp:302-364; Dirichlet
+// increments solver.cpp:111-116) for the row and feeds it straight into the
+// segment elimination of I - th L_r (assemble_line_r, discretization.cpp:194-230;
+// Thomas solver.cpp:22-57 by the partition method). Face rows j = 0, nv-1
+// (block-uniform) take the generic out-of-line stencil. Columns on v/y
+// Dirichlet faces (not solved, solver.cpp:127) run identity rows, so dU1 = dU0.
+constexpr int kRing = 4;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int NV, int NY>
+__global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
+    constexpr int M = 16;
+    constexpr int SR = NV * NY;
+    extern __shared__ double sm[];
+    const int S = blockDim.y;
+    const int nt = 16 * S;
+    double* red = sm;                          // [16][S][8] reduced-system rows
+    double* ring = red + nt * 8;               // [kRing][3][nt] window prefetch
+    double* rt = ring + kRing * 3 * nt;        // [nr][8] r-table (FastR)
+    const int p = blockIdx.y;
+    DevStatus& st = v.st[p];
+    if (st.fail_step) return;
+    const int nr = v.nr;
+    const int tx = threadIdx.x, sg = threadIdx.y;
+    const int tid = sg * 16 + tx;
+    constexpr int TK = NY / 16;
+    const int j = blockIdx.x / TK;
+    const int k = (blockIdx.x - j * TK) * 16 + tx;
+    if (blockIdx.x == 0 && tid == 0) st.maxdelta_bits = 0ull;
+    const ProblemConst& pc = v.pc[p];
+    const bool yminD = dir(v, F_YMIN), ymaxD = dir(v, F_YMAX);
+    const bool k0 = k == 0, kN = k == NY - 1;
+    const unsigned hmask = 0xffffu << ((sg & 1) * 16);  // this half-warp (blockDim.x == 16)
+    // is_dirichlet(1,j,k) (solver.cpp:127): the column lies on a v or y Dirichlet face
+    const bool solve = !(kN && ymaxD) && !(j == NV - 1 && dir(v, F_VMAX)) && !(k0 && yminD) &&
+                       !(j == 0 && dir(v, F_VMIN));
+    const int a = sg * M;
+    const size_t off = static_cast<size_t>(p) * v.N;
+    const FT F = ftab(v, p);
+    for (int e = tid; e < nr * kFR / 2; e += nt)
+        reinterpret_cast<double2*>(rt)[e] = __ldg(reinterpret_cast<const double2*>(F.R) + e);
+    const double c4 = __ldg(step_row(v, p, s) + ST_C4);
+    const double2* V2 = reinterpret_cast<const double2*>(F.V + kFV * j);
+    const double2 v01 = __ldg(V2), v23 = __ldg(V2 + 1);  // (V, G2), (G5, G3V)
+    const double2* Y2 = reinterpret_cast<const double2*>(F.Y + kFY * k);
+    const double2 y01 = __ldg(Y2), y23 = __ldg(Y2 + 1);  // (S6, T6), (Y, pad)
+    const double vj = v01.x, yk = y23.x;
+    const double vs6 = vj * y01.x, t6 = y01.y;
+    const double th = pc.theta_dt, dtm = pc.dt;
+    const bool rmaxD = dir(v, F_RMAX), rminD = dir(v, F_RMIN);
+    const bool slowj = j == 0 || j == NV - 1;  // block-uniform
+    const bool order2y = v.y_order != 1, order2r = v.r_order != 1;
+    const double* fbp = v.fb + static_cast<size_t>(p) * v.fb_stride;
+    const double* fby = fbp + 2 * NY + (kN ? 0 : nr);
+    const bool kface = (kN && ymaxD) || (k0 && yminD);
+    const double* __restrict__ col = v.U + off + static_cast<size_t>(j) * NY + k;
+    double x[M], cs[M], al[M];
+    __syncthreads();  // rt
+
+    // row coefficients of I - th L_r at row i (g4h shared with the stencil)
+    auto coeffs = [&](int i, double g1s, double g4h, double& l, double& d, double& u, double& s2) {
+        l = 0.0; d = 1.0; u = 0.0; s2 = 0.0;
+        if (!solve || (i == nr - 1 && rmaxD) || (i == 0 && rminD)) return;
+        if (i == 0) {
+            if (!order2r) {
+                d = fma(2.0 * th, g4h, 1.0);
+                u = -2.0 * th * g4h;
+            } else {
+                d = fma(3.0 * th, g4h, 1.0);
+                u = -4.0 * th * g4h;
+                s2 = th * g4h;
+            }
+        } else {
+            const double w2 = th * g1s, w1 = th * g4h;
+            l = w1 - w2;
+            d = fma(2.0, w2, 1.0);
+            u = -(w2 + w1);
+        }
+    };
+    auto rtab = [&](int i, double2& r01, double2& r23, double2& r45, double2& r67) {
+        const double2* R2 = reinterpret_cast<const double2*>(rt + kFR * i);
+        r01 = R2[0]; r23 = R2[1]; r45 = R2[2]; r67 = R2[3];
+        // r01 = (G1, G4C), r23 = (G4P, G4Q), r45 = (G4V, G3), r67 = (REACT, A)
+    };
+    auto g4 = [&](const double2& r01, const double2& r23, const double2& r45) {
+        return fma(c4, r01.y, fma(r23.y, yk, fma(r45.x, vj, r23.x)));
+    };
+
+    double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
+    int bad_r = 0;
+    bool ok = true;
+    if (slowj) {
+        // face rows j = 0 / nv-1: generic stencil per node, then the plain segment solve
+#pragma unroll
+        for (int r = 0; r < M; ++r) x[r] = explicit_slow(v, p, s, a + r, j, k);
+        double f0d = 1.0, f0u = 0.0;
+        if (a == 0) {
+            double2 r01, r23, r45, r67;
+            rtab(0, r01, r23, r45, r67);
+            double l0, d0, u0, s20, l1, d1, u1, t1;
+            coeffs(0, r01.x * vj, g4(r01, r23, r45), l0, d0, u0, s20);
+            f0d = d0;
+            f0u = u0;
+            if (s20 != 0.0) {
+                rtab(1, r01, r23, r45, r67);
+                coeffs(1, r01.x * vj, g4(r01, r23, r45), l1, d1, u1, t1);
+                if (fabs(u1) > 1e-300) {
+                    const double f = s20 / u1;
+                    f0d = fma(-f, l1, d0);
+                    f0u = fma(-f, d1, u0);
+                    x[0] = fma(-f, x[1], x[0]);
+                } else {
+                    x[0] = fma(-s20, x[2], x[0]);
+                }
+            }
+        }
+        auto row = [&](int r, double& l, double& d, double& u) {
+            if (a == 0 && r == 0) {
+                l = 0.0; d = f0d; u = f0u;
+                return;
+            }
+            double2 r01, r23, r45, r67;
+            rtab(a + r, r01, r23, r45, r67);
+            double s2;
+            coeffs(a + r, r01.x * vj, g4(r01, r23, r45), l, d, u, s2);
+        };
+        ok = seg_solve<M>(M, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
+    } else {
+        // window for columns j-1 (0), j (1), j+1 (2): m = row ic-1, c = ic, p = ic+1;
+        // rows ic+2 .. ic+1+kRing are in flight in this thread's ring slots
+        auto gptr = [&](int ii) { return col + static_cast<size_t>(min(max(ii, 0), nr - 1)) * SR; };
+        auto slot = [&](int q, int c) { return ring + (q * 3 + c) * nt + tid; };
+        double m0, m1, m2, c0, c1, c2, p0, p1, p2;
+        {
+            const double* q = gptr(a - 1);
+            m0 = __ldg(q - NY); m1 = __ldg(q); m2 = __ldg(q + NY);
+            q = gptr(a);
+            c0 = __ldg(q - NY); c1 = __ldg(q); c2 = __ldg(q + NY);
+            q = gptr(a + 1);
+            p0 = __ldg(q - NY); p1 = __ldg(q); p2 = __ldg(q + NY);
+        }
+#pragma unroll
+        for (int q = 0; q < kRing; ++q) {
+            const double* g = gptr(a + 2 + q);
+            cp_async8(slot(q, 0), g - NY);
+            cp_async8(slot(q, 1), g);
+            cp_async8(slot(q, 2), g + NY);
+            cp_async_commit();
+        }
+        // centre moves to row a+r: row a+r+1 comes out of ring slot (r-1) % kRing,
+        // which is refilled with row a+r+kRing+1
+        auto shift = [&](int r) {
+            const int q = (r - 1) % kRing;
+            cp_async_wait<kRing - 1>();
+            m0 = c0; m1 = c1; m2 = c2;
+            c0 = p0; c1 = p1; c2 = p2;
+            p0 = *slot(q, 0); p1 = *slot(q, 1); p2 = *slot(q, 2);
+            const double* g = gptr(a + r + kRing + 1);
+            cp_async8(slot(q, 0), g - NY);
+            cp_async8(slot(q, 1), g);
+            cp_async8(slot(q, 2), g + NY);
+            cp_async_commit();
+        };
+        // y-direction terms and the k faces (discretization.cpp:340-352)
+        auto yterm = [&](int i, double u0, double acc, double a_i) {
+            double kl = __shfl_up_sync(hmask, u0, 1, 16);
+            double kr = __shfl_down_sync(hmask, u0, 1, 16);
+            const double* q = col + static_cast<size_t>(i) * SR;
+            if (tx == 0 && !k0) kl = __ldg(q - 1);
+            if (tx == 15 && !kN) kr = __ldg(q + 1);
+            double yd = kr - kl;
+            if (k0) {  // one-sided y row (discretization.cpp:346-352)
+                const double k2 = __ldg(q + 2);
+                yd = order2y ? fma(4.0, kr, -k2) - 3.0 * u0 : 2.0 * (kr - u0);
+            }
+            acc = fma(fma(a_i, vs6, t6), yd, acc);
+            double out = acc * dtm;
+            if (kface) out = __ldg(fby + i) - u0;
+            return out;
+        };
+        // dU0 at an interior row i from a window (mm, cc, pp)
+        auto stencil = [&](int i, const double2& r01, const double2& r45, const double2& r67,
+                           double g4h, double mq0, double mq1, double mq2, double cq0, double cq1,
+                           double cq2, double pq0, double pq1, double pq2) {
+            const double u0 = cq1;
+            double acc = -r67.x * u0;
+            acc = fma(r01.x * vj, (pq1 + mq1) - 2.0 * u0, acc);
+            acc = fma(g4h, pq1 - mq1, acc);
+            acc = fma(v01.y, (cq2 + cq0) - 2.0 * u0, acc);
+            acc = fma(v23.x, cq2 - cq0, acc);
+            acc = fma(r45.y * v23.y, (pq2 - pq0) - (mq2 - mq0), acc);
+            return yterm(i, u0, acc, r67.y);
+        };
+        auto row = [&](int r, double& l, double& d, double& u) {
+            const int i = a + r;
+            double2 r01, r23, r45, r67;
+            rtab(i, r01, r23, r45, r67);
+            const double g4h = g4(r01, r23, r45);
+            double s2;
+            if (r == 0) {
+                if (a == 0) {
+                    // face plane i = 0 (discretization.cpp:318-329): one-sided g4 term, no cross
+                    cp_async_wait<kRing - 1>();  // row 2 (ring slot 0)
+                    const double n0 = *slot(0, 0), n1 = *slot(0, 1), n2 = *slot(0, 2);
+                    const double u0 = c1;
+                    double acc = -r67.x * u0;
+                    acc = fma(g4h, order2r ? fma(4.0, p1, -n1) - 3.0 * u0 : 2.0 * (p1 - u0), acc);
+                    acc = fma(v01.y, (c2 + c0) - 2.0 * u0, acc);
+                    acc = fma(v23.x, c2 - c0, acc);
+                    double x0 = yterm(0, u0, acc, r67.y);
+                    // r_min Dirichlet ranks below r_max / y_max / v_max (discretization.cpp:153-192)
+                    if (rminD && !(kN && ymaxD)) x0 = __ldg(fbp + NY + k) - u0;
+                    x[0] = x0;
+                    // the super2 fold needs row 1's rhs (solver.cpp:28-40)
+                    double2 q01, q23, q45, q67;
+                    rtab(1, q01, q23, q45, q67);
+                    const double g4h1 = g4(q01, q23, q45);
+                    const double x1 = stencil(1, q01, q45, q67, g4h1, c0, c1, c2, p0, p1, p2, n0, n1, n2);
+                    double d0, u0c, s20, l1, d1, u1, t1, l0;
+                    coeffs(0, r01.x * vj, g4h, l0, d0, u0c, s20);
+                    double f0d = d0, f0u = u0c;
+                    if (s20 != 0.0) {
+                        coeffs(1, q01.x * vj, g4h1, l1, d1, u1, t1);
+                        if (fabs(u1) > 1e-300) {
+                            const double f = s20 / u1;
+                            f0d = fma(-f, l1, d0);
+                            f0u = fma(-f, d1, u0c);
+                            x[0] = fma(-f, x1, x[0]);
+                        } else {  // lagged fold: row 2's rhs (rows 1..3 of the window)
+                            cp_async_wait<kRing - 2>();
+                            double2 w01, w23, w45, w67;
+                            rtab(2, w01, w23, w45, w67);
+                            const double x2 = stencil(2, w01, w45, w67, g4(w01, w23, w45), p0, p1, p2, n0,
+                                                      n1, n2, *slot(1, 0), *slot(1, 1), *slot(1, 2));
+                            x[0] = fma(-s20, x2, x[0]);
+                        }
+                    }
+                    l = 0.0; d = f0d; u = f0u;
+                    return;
+                }
+                x[0] = stencil(i, r01, r45, r67, g4h, m0, m1, m2, c0, c1, c2, p0, p1, p2);
+            } else {
+                shift(r);
+                const double xv = stencil(i, r01, r45, r67, g4h, m0, m1, m2, c0, c1, c2, p0, p1, p2);
+                // face plane i = nr-1: r_max is always Dirichlet and ranks first
+                x[r] = (r == M - 1 && i == nr - 1 && rmaxD) ? __ldg(fbp + k) - c1 : xv;
+            }
+            coeffs(i, r01.x * vj, g4h, l, d, u, s2);
+        };
+        ok = seg_solve<M>(M, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
+        cp_async_wait<0>();
+    }
+    if (!ok) record_pivot(st, s, 0, j * NY + k, a + bad_r);
+    double* E = red + (tx * S + sg) * 8;
+    E[0] = yF; E[1] = aF; E[2] = bF; E[3] = yL; E[4] = aL; E[5] = bL;
+    __syncthreads();
+    if (sg == 0 && solve && S > 1) {
+        int bt = 0;
+        if (!reduced_solve(red + tx * S * 8, S, 8, bt)) record_pivot(st, s, 0, j * NY + k, bt * M);
+    }
+    __syncthreads();
+    const double left = (solve && sg > 0) ? E[-8 + 6] : 0.0;  // p_{s-1} = x_{a-1}
+    const double right = (solve && sg < S - 1) ? E[7] : 0.0;  // q_s = x_{a+m}
+    double b = bL;
+    double* __restrict__ dcol = v.D + off + static_cast<size_t>(j) * NY + k + static_cast<size_t>(a) * SR;
+#pragma unroll
+    for (int r = M - 1; r >= 0; --r) {
+        if (r < M - 1) b = -cs[r] * b;
+        dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(al[r], left, x[r]));
+    }
+}
+
+inline size_t pa_smem(int nr) {
+    const int S = nr / 16, nt = 16 * S;
+    return sizeof(double) * (static_cast<size_t>(nt) * 8 + static_cast<size_t>(kRing) * 3 * nt +
+                             static_cast<size_t>(nr) * kFR);
+}
+
+// ------------------------------------------------------------ pass B, fused plane
+// A cluster of CS CTAs per (problem, plane i); CTA c holds rows j in
+// [c*RV, (c+1)*RV) of the plane of dU1 in shared memory. The v-lines (columns
+// k) are solved by segmented affine scans of the table LU: every CTA scans its
+// own 16-row segments, broadcasts the segment end values to all CTAs of the
+// cluster through distributed shared memory, and each CTA then runs the (short)
+// carry chain over all segments itself. The y-lines (rows j, CTA-local) use the
+// partition method (16-row segments, per-line reduced systems inside a warp),
+// and each y-segment finishes straight into U += dU3, Dirichlet re-imposition,
+// max|dU| and the guard (solver.cpp:136-176).
+// Element (j,k) lives at j*PITCH + (k/16)*17 + k%16: both the column walks
+// (lanes = k) and the segment walks (lanes = segments) are at most 2-way bank
+// conflicted.
+template <int NV, int NY, int CS, int NTX>
+struct PlaneGeom {
+    static constexpr int MS = 16;                 // rows per segment (v and y)
+    static constexpr int RV = NV / CS;            // rows j per CTA
+    static constexpr int LY = NY / MS;            // y segments per line
+    static constexpr int SV = NV / MS;            // v segments per column
+    static constexpr int SVL = RV / MS;           // v segments per CTA
+    static constexpr int P0 = LY * 17;
+    static constexpr int PITCH = P0 + ((8 - (P0 % 16)) + 16) % 16;  // = 8 (mod 16)
+    static constexpr int NT = NTX;
+    static constexpr int YROUNDS = (RV * LY + NT - 1) / NT;
+    static constexpr int TILE = RV * PITCH;
+    static constexpr int VT = 5 * NV;             // v tables: RP B E BF BB
+    static constexpr int YT = 2 * (LY * 17);      // y tables: (S6, T6) pairs, 17-pair segments
+    static constexpr int CAR = 2 * SV * NY;       // v carries (all segments, both directions)
+    static constexpr int EY = NT * 8;             // y reduced-system rows per round
+    static constexpr size_t SMEM = sizeof(double) * (TILE + VT + YT + CAR + EY);
+    // CTAs per SM the shared memory allows, capped at 128 registers per thread
+    static constexpr int BY_SMEM = static_cast<int>((227 * 1024) / (SMEM + 1024));
+    static constexpr int MINB = (512 / NT) < BY_SMEM ? (512 / NT) : (BY_SMEM > 0 ? BY_SMEM : 1);
+    static_assert(RV % MS == 0 && NY % MS == 0, "segments must tile the plane");
+    static_assert(32 % LY == 0 && NT % 32 == 0, "y-lines must not straddle warps");
+    static_assert((RV * NY / 2) % NT == 0, "plane rows must split evenly over the block");
+    __device__ static int at(int j, int k) { return j * PITCH + (k >> 4) * 17 + (k & 15); }
+};
+
+template <int NV, int NY, int CS, int NTX>
+__global__ void __launch_bounds__(NTX, (PlaneGeom<NV, NY, CS, NTX>::MINB))
+k_plane(BatchView v, int s) {
+    using G = PlaneGeom<NV, NY, CS, NTX>;
+    constexpr int MS = G::MS, LY = G::LY, SV = G::SV, SVL = G::SVL, RV = G::RV, NT = G::NT;
+    extern __shared__ double sm[];
+    double* tile = sm;
+    double* vtab = tile + G::TILE;   // [5][NV]: RP, B, E, BF, BB
+    double* ytab = vtab + G::VT;     // [LY*17] (S6, T6) pairs
+    double* car = ytab + G::YT;      // [2][SV][NY]
+    double* ey = car + G::CAR;       // [NT/LY lines][LY][8]
+    const int nr = v.nr;
+    const int tid = threadIdx.x;
+    const int w = blockIdx.x / CS;
+    const int c = CS > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+    const int j0 = c * RV;
+    const int p = w / nr, i = w - (w / nr) * nr;
+    DevStatus& st = v.st[p];
+    // a failed problem skips the work but still takes part in the cluster barriers
+    const bool live_p = st.fail_step == 0;
+    auto cluster_sync = [] {
+        if constexpr (CS > 1) cg::this_cluster().sync();
+        else __syncthreads();
+    };
+    auto bcast = [&](int idx, double val) {  // write car[idx] in every CTA of the cluster
+        if constexpr (CS > 1) {
+#pragma unroll
+            for (int r = 0; r < CS; ++r) cg::this_cluster().map_shared_rank(car, r)[idx] = val;
+        } else {
+            car[idx] = val;
+        }
+    };
+    const size_t off = static_cast<size_t>(p) * v.N;
+    const size_t pb = off + (static_cast<size_t>(i) * NV + j0) * NY;  // first row of this CTA
+    const FT F = ftab(v, p);
+    if (live_p) {
+        if (tid == 0) {  // U rows -> L2 early, so the update's loads hit L2
+            constexpr unsigned bytes = RV * NY * sizeof(double);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.U + pb), "r"(bytes) : "memory");
+        }
+        // stage the rows of dU1: all 128-bit loads in flight, then the smem stores
+        constexpr int PER = RV * NY / 2 / NT;
+        const double2* src = reinterpret_cast<const double2*>(v.D + pb);
+        double2 t[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) t[q] = __ldg(src + q * NT + tid);
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int e = q * NT + tid;
+            const int j = (2 * e) / NY, k = 2 * e - j * NY;
+            tile[G::at(j, k)] = t[q].x;
+            tile[G::at(j, k + 1)] = t[q].y;
+        }
+        for (int e = tid; e < NV; e += NT) {
+            const double* Vr = F.V + kFV * e;
+            vtab[e] = Vr[FV_RP];
+            vtab[NV + e] = Vr[FV_B];
+            vtab[2 * NV + e] = Vr[FV_E];
+            vtab[3 * NV + e] = Vr[FV_BF];
+            vtab[4 * NV + e] = Vr[FV_BB];
+        }
+        for (int e = tid; e < NY; e += NT) {  // padded so the segments hit distinct banks
+            const int cc = 2 * ((e >> 4) * 17 + (e & 15));
+            ytab[cc] = F.Y[kFY * e + FY_S6];
+            ytab[cc + 1] = F.Y[kFY * e + FY_T6];
+        }
+    }
+    __syncthreads();
+    const bool planeD = (i == nr - 1 && dir(v, F_RMAX)) || (i == 0 && dir(v, F_RMIN));
+    const bool yminD = dir(v, F_YMIN), ymaxD = dir(v, F_YMAX);
+    const bool vminD = dir(v, F_VMIN), vmaxD = dir(v, F_VMAX);
+    const bool vwork = live_p && !planeD;
+
+    // ---- v-lines (columns k), skip columns on y Dirichlet faces (solver.cpp:142)
+    if (!planeD) {  // uniform over the cluster
+        if (vwork) {
+            for (int task = tid; task < NY * SVL; task += NT) {
+                const int k = task % NY, sl = task / NY, a = sl * MS;
+                if ((k == 0 && yminD) || (k == NY - 1 && ymaxD)) continue;
+                double loc = 0.0;
+                int bad = -1;
+#pragma unroll
+                for (int r = 0; r < MS; ++r) {  // local forward scan
+                    const int jg = j0 + a + r;
+                    if (isnan(vtab[jg]) && bad < 0) bad = jg;  // singular v pivot (table NaN)
+                    loc = fma(vtab[NV + jg], loc, vtab[jg] * tile[G::at(a + r, k)]);
+                    tile[G::at(a + r, k)] = loc;
+                }
+                bcast((c * SVL + sl) * NY + k, loc);
+                if (bad >= 0) record_pivot(st, s, 1, i * NY + k, bad);
+            }
+        }
+        cluster_sync();
+        if (vwork) {
+            for (int k = tid; k < NY; k += NT) {  // forward carries over all segments
+                double cc = 0.0;
+#pragma unroll
+                for (int t = 0; t < SV; ++t) {
+                    const double endv = car[t * NY + k];
+                    car[t * NY + k] = cc;
+                    cc = fma(vtab[3 * NV + (t * MS + MS - 1)], cc, endv);
+                }
+            }
+        }
+        __syncthreads();
+        if (vwork) {
+            for (int task = tid; task < NY * SVL; task += NT) {
+                const int k = task % NY, sl = task / NY, a = sl * MS;
+                if ((k == 0 && yminD) || (k == NY - 1 && ymaxD)) continue;
+                const int sv = c * SVL + sl;
+                const double cin = car[sv * NY + k];
+                double xb = 0.0;
+#pragma unroll
+                for (int r = MS - 1; r >= 0; --r) {  // fix dp, local backward scan
+                    const int jg = j0 + a + r;
+                    const double dp = fma(vtab[3 * NV + jg], cin, tile[G::at(a + r, k)]);
+                    xb = fma(vtab[2 * NV + jg], xb, dp);
+                    tile[G::at(a + r, k)] = xb;
+                }
+                bcast(SV * NY + sv * NY + k, xb);
+            }
+        }
+        cluster_sync();
+        if (vwork) {
+            for (int k = tid; k < NY; k += NT) {  // backward carries from the top
+                double cc = 0.0;
+#pragma unroll
+                for (int t = SV - 1; t >= 0; --t) {
+                    const double firstv = car[SV * NY + t * NY + k];
+                    car[SV * NY + t * NY + k] = cc;
+                    cc = fma(vtab[4 * NV + t * MS], cc, firstv);
+                }
+            }
+        }
+        __syncthreads();
+        if (vwork) {
+            for (int task = tid; task < NY * SVL; task += NT) {
+                const int k = task % NY, sl = task / NY, a = sl * MS;
+                if ((k == 0 && yminD) || (k == NY - 1 && ymaxD)) continue;
+                const double cout = car[SV * NY + (c * SVL + sl) * NY + k];
+#pragma unroll
+                for (int r = 0; r < MS; ++r)
+                    tile[G::at(a + r, k)] = fma(vtab[4 * NV + j0 + a + r], cout, tile[G::at(a + r, k)]);
+            }
+        }
+        __syncthreads();
+    }
+    if (!live_p) return;  // no cluster barrier follows
+
+    // ---- y-lines (rows j) + update, in rounds of NT segment tasks
+    const ProblemConst& pc = v.pc[p];
+    const double th = pc.theta_dt;
+    const double a_i = F.R[kFR * i + FR_A], react = F.R[kFR * i + FR_REACT];
+    const double dint = fma(th, react, 1.0);
+    const double bound = pc.bound;
+    const double* fby = v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY;  // y faces [nr] x2
+    double md = 0.0;
+#pragma unroll 1
+    for (int h = 0; h < G::YROUNDS; ++h) {
+        const int task = h * NT + tid;
+        const bool live = task < RV * LY;
+        const int jl = live ? task / LY : 0, sy = task % LY;
+        const int j = j0 + jl;
+        const int a = sy * MS;
+        const bool solve = live && !planeD && !((j == 0 && vminD) || (j == NV - 1 && vmaxD));
+        double x[MS], cs[MS], al[MS];
+#pragma unroll
+        for (int r = 0; r < MS; ++r) x[r] = live ? tile[G::at(jl, a + r)] : 0.0;
+        double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
+        if (solve) {
+            const double h1 = a_i * F.V[kFV * j + FV_V];
+            double lr[MS];
+            double g60 = 0.0;
+#pragma unroll
+            for (int r = 0; r < MS; ++r) {
+                const double2 st6 = reinterpret_cast<const double2*>(ytab)[sy * 17 + r];
+                const double g6h = fma(h1, st6.x, st6.y);
+                if (r == 0) g60 = g6h;
+                lr[r] = th * g6h;
+            }
+            double f0d = dint, f0u = -lr[0];
+            if (sy == 0) {  // row 0 (discretization.cpp:274-289), folded (solver.cpp:28-40)
+                f0d = 1.0;
+                f0u = 0.0;
+                if (!yminD) {
+                    if (v.y_order == 1) {
+                        f0d = fma(th, fma(2.0, g60, react), 1.0);
+                        f0u = -2.0 * lr[0];
+                    } else {
+                        f0d = fma(th, fma(3.0, g60, react), 1.0);
+                        f0u = -4.0 * lr[0];
+                        const double s20 = lr[0];
+                        const double l1 = lr[1], u1 = -lr[1];
+                        if (fabs(u1) > 1e-300) {
+                            const double f = s20 / u1;
+                            f0d = fma(-f, l1, f0d);
+                            f0u = fma(-f, dint, f0u);
+                            x[0] = fma(-f, x[1], x[0]);
+                        } else {
+                            x[0] = fma(-s20, x[2], x[0]);
+                        }
+                    }
+                }
+            }
+            const bool lastI = sy == LY - 1 && ymaxD;
+            auto row = [&](int r, double& l, double& d, double& u) {
+                if (r == 0 && sy == 0) {
+                    l = 0.0; d = f0d; u = f0u;
+                } else if (r == MS - 1 && lastI) {
+                    l = 0.0; d = 1.0; u = 0.0;
+                } else {
+                    l = lr[r]; d = dint; u = -lr[r];
+                }
+            };
+            int bad_r = 0;
+            if (!seg_solve<MS>(MS, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row))
+                record_pivot(st, s, 2, i * NV + j, a + bad_r);
+        }
+        const int lslot = (tid / LY) * LY * 8 + sy * 8;  // line-local slot in ey
+        if (live) {
+            double* e = ey + lslot;
+            e[0] = yF; e[1] = aF; e[2] = bF; e[3] = yL; e[4] = aL; e[5] = bL;
+        }
+        __syncwarp();  // a line's LY segments lie in one warp
+        if (solve && sy == 0 && LY > 1) {
+            int bt = 0;
+            if (!reduced_solve(ey + lslot, LY, 8, bt)) record_pivot(st, s, 2, i * NV + j, bt * MS);
+        }
+        __syncwarp();
+        if (live) {
+            const double left = (solve && sy > 0) ? ey[lslot - 8 + 6] : 0.0;
+            const double right = (solve && sy < LY - 1) ? ey[lslot + 7] : 0.0;
+            double* up = v.U + pb + static_cast<size_t>(jl) * NY + a;
+            double un[MS];
+#pragma unroll
+            for (int q = 0; q < MS / 2; ++q) {
+                const double2 t = reinterpret_cast<const double2*>(up)[q];
+                un[2 * q] = t.x;
+                un[2 * q + 1] = t.y;
+            }
+            double b = bL;
+#pragma unroll
+            for (int r = MS - 1; r >= 0; --r) {
+                double dq = x[r];
+                if (solve) {
+                    if (r < MS - 1) b = -cs[r] * b;
+                    dq = fma(b, right, fma(al[r], left, x[r]));
+                }
+                un[r] += dq;
+                md = fmax(md, fabs(dq));
+            }
+            if (!solve) {
+#pragma unroll
+                for (int r = 0; r < MS; ++r) un[r] = fval(v, p, dface(v, i, j, a + r), i, a + r);
+            } else {
+                if (sy == 0 && yminD) un[0] = __ldg(fby + nr + i);
+                if (sy == LY - 1 && ymaxD) un[MS - 1] = __ldg(fby + i);
+            }
+#pragma unroll
+            for (int r = 0; r < MS; ++r)
+                if (!(fabs(un[r]) <= bound))
+                    guard_fail(v, p, s, (static_cast<size_t>(i) * NV + j) * NY + a + r, un[r]);
+#pragma unroll
+            for (int q = 0; q < MS / 2; ++q)
+                reinterpret_cast<double2*>(up)[q] = make_double2(un[2 * q], un[2 * q + 1]);
+        }
+        __syncwarp();  // ey is reused by the next round
+    }
+    for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+    if ((tid & 31) == 0 && md > 0.0)
+        atomicMax(&st.maxdelta_bits, static_cast<unsigned long long>(__double_as_longlong(md)));
+}
+
+template <int NV, int NY, int CS, int NT>
+void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
+    using G = PlaneGeom<NV, NY, CS, NT>;
+    static const bool attr = [] {
+        cudaFuncSetAttribute(k_plane<NV, NY, CS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(G::SMEM));
+        return true;
+    }();
+    (void)attr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(v.nr * v.P * CS);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = G::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_plane<NV, NY, CS, NT>, v, s);
+}
+
+int plane_kernels() {
+    static const int on = [] {
+        const char* e = std::getenv("HJMSV_PLANE");
+        return e ? std::atoi(e) : 1;
+    }();
+    return on;
+}
+
 }  // namespace
 
 // (nv, ny) pairs with compile-time kernels: nv == ny in {32, 64, 128, 256}
@@ -1115,33 +1752,58 @@ void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launch
     const int shape = specialised_shape(v);
     k_faces<<<dim3((v.fb_stride + 255) / 256, v.P), 256, 0, stream>>>(v, s);
     mark(4, "fx_faces", 0.0);
-    constexpr int TI = 8;
-    const dim3 gex(tk * tj, (v.nr + TI - 1) / TI, v.P);
-    static const int exv = [] {
-        const char* e = std::getenv("HJMSV_EX_MINB");
-        return e ? std::atoi(e) : 0;
+    static const int pa_env = [] {
+        const char* e = std::getenv("HJMSV_PA");
+        return e ? std::atoi(e) : 1;
     }();
-#define HJ_EX(NVV, MB) k_ex3<NVV, NVV, TI, MB><<<gex, dim3(32, 8), 0, stream>>>(v, s)
-#define HJ_EXS(NVV)                   \
-    if (exv == 0) k_ex4<NVV, NVV><<<dim3(tk * tj, v.nr, v.P), dim3(32, 8), 0, stream>>>(v, s); \
-    else if (exv >= 4) HJ_EX(NVV, 4);       \
-    else if (exv == 3) HJ_EX(NVV, 3);  \
-    else HJ_EX(NVV, 2)
-    switch (shape) {
-        case 32: HJ_EXS(32); break;
-        case 64: HJ_EXS(64); break;
-        case 128: HJ_EXS(128); break;
-        case 256: HJ_EXS(256); break;
-        default: k_fx_explicit<<<dim3(tk * tj, v.nr, v.P), dim3(32, 8), 0, stream>>>(v, s);
+    if (pa_env && shape != 0 && v.nr % 16 == 0 && v.nr / 16 <= 32) {
+        // pass A fused: explicit stencil + r-lines
+        const int S = v.nr / 16;
+        const dim3 g(v.nv * (v.ny / 16), v.P), b(16, S);
+        const size_t sm = pa_smem(v.nr);
+        static const bool attr = [] {
+            const int mx = static_cast<int>(pa_smem(512));
+            cudaFuncSetAttribute(k_pa<32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_pa<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_pa<128, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_pa<256, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            return true;
+        }();
+        (void)attr;
+        switch (shape) {
+            case 32: k_pa<32, 32><<<g, b, sm, stream>>>(v, s); break;
+            case 64: k_pa<64, 64><<<g, b, sm, stream>>>(v, s); break;
+            case 128: k_pa<128, 128><<<g, b, sm, stream>>>(v, s); break;
+            default: k_pa<256, 256><<<g, b, sm, stream>>>(v, s); break;
+        }
+        mark(0, "fx_explicit_sweep_r", 16.0);
+    } else {
+        switch (shape) {
+            case 32: k_ex4<32, 32><<<dim3(tk * tj, v.nr, v.P), dim3(32, 8), 0, stream>>>(v, s); break;
+            case 64: k_ex4<64, 64><<<dim3(tk * tj, v.nr, v.P), dim3(32, 8), 0, stream>>>(v, s); break;
+            case 128: k_ex4<128, 128><<<dim3(tk * tj, v.nr, v.P), dim3(32, 8), 0, stream>>>(v, s); break;
+            case 256: k_ex4<256, 256><<<dim3(tk * tj, v.nr, v.P), dim3(32, 8), 0, stream>>>(v, s); break;
+            default: k_fx_explicit<<<dim3(tk * tj, v.nr, v.P), dim3(32, 8), 0, stream>>>(v, s);
+        }
+        mark(0, "fx_explicit", 16.0);
+        const int Sr = (v.nr + kSegR - 1) / kSegR;
+        const int tkr = (v.ny + kLanesR - 1) / kLanesR;
+        k_fx_r<kSegR><<<dim3(v.nv * tkr, v.P), dim3(kLanesR, Sr),
+                        static_cast<size_t>(kLanesR) * Sr * 8 * sizeof(double), stream>>>(v, s);
+        mark(1, "fx_sweep_r", 16.0);
     }
-#undef HJ_EXS
-#undef HJ_EX
-    mark(0, "fx_explicit", 16.0);
-    const int Sr = (v.nr + kSegR - 1) / kSegR;
-    const int tkr = (v.ny + kLanesR - 1) / kLanesR;
-    k_fx_r<kSegR><<<dim3(v.nv * tkr, v.P), dim3(kLanesR, Sr),
-                    static_cast<size_t>(kLanesR) * Sr * 8 * sizeof(double), stream>>>(v, s);
-    mark(1, "fx_sweep_r", 16.0);
+    const int pl = plane_kernels();
+    if (pl && (shape == 32 || shape == 64 || shape == 128 || (shape == 256 && pl == 3))) {
+        // pass B fused: v-lines + y-lines + update on an SMEM-resident plane
+        if (shape == 32) launch_plane<32, 32, 1, 64>(v, s, stream);
+        else if (shape == 64) launch_plane<64, 64, 1, 256>(v, s, stream);
+        else if (shape == 128) {
+            if (pl == 3) launch_plane<128, 128, 2, 256>(v, s, stream);
+            else launch_plane<128, 128, 1, 256>(v, s, stream);
+        } else launch_plane<256, 256, 8, 256>(v, s, stream);
+        mark(2, "fx_plane_vy_update", 24.0);
+        return;
+    }
     const int Sv = (v.nv + kSegV - 1) / kSegV;
     k_fx_v<<<dim3(v.nr * tk, v.P), dim3(32, Sv), 2ull * Sv * 32 * sizeof(double), stream>>>(v, s);
     mark(2, "fx_sweep_v", 16.0);
