@@ -128,8 +128,9 @@ namespace {
 
 void enqueue_steps(hjmsv_solver* h, int from, int count, long long* launches) {
     for (int s = from; s < from + count; ++s) {
+        const int flags = (s == from ? STEP_FIRST : 0) | (s == from + count - 1 ? STEP_LAST : 0);
         if (h->mode == HJMSV_MODE_FAST)
-            fast_step(h->view, s, h->stream, launches);
+            fast_step(h->view, s, h->stream, launches, nullptr, flags);
         else
             strict_step(h->view, s, h->stream, launches);
     }
@@ -310,7 +311,7 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         h->fast = dalloc<double>(static_cast<size_t>(count) * v.fast_stride);
         v.fast = h->fast;
         v.fb_stride = 2 * h->ny + 2 * h->nr + 2 * h->nr * h->ny;
-        h->fb = dalloc<double>(static_cast<size_t>(count) * v.fb_stride);
+        h->fb = dalloc<double>(2 * static_cast<size_t>(count) * v.fb_stride);  // two step parities
         v.fb = h->fb;
         for (int p = 0; p < count; ++p) {
             const std::vector<double> ft = build_fast_tables(L[p], cfg, L[p].pc.theta_dt);
@@ -379,8 +380,9 @@ int32_t hjmsv_solver_kernel_profile(hjmsv_solver* h, int32_t steps, int32_t max_
         CK(cudaEventRecord(start, h->stream));
         long long n = 0;
         for (int s = h->step; s < h->step + count; ++s) {
+            const int flags = (s == h->step ? STEP_FIRST : 0) | (s == h->step + count - 1 ? STEP_LAST : 0);
             if (h->mode == HJMSV_MODE_FAST)
-                fast_step(h->view, s, h->stream, &n, &hook);
+                fast_step(h->view, s, h->stream, &n, &hook, flags);
             else
                 strict_step(h->view, s, h->stream, &n, &hook);
         }

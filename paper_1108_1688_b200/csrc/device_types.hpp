@@ -69,7 +69,13 @@ struct BatchView {
     int dmask;            // bit f set when face f is Dirichlet (uniform across the batch)
     double* fb;           // [P][fb_stride] Dirichlet face values at t_next of the current step
     int fb_stride;        // 2ny (r faces) + 2nr (y faces) + 2 nr ny (v faces)
+    double* fb_next;      // [P][fb_stride] the next step's values (filled by the last kernel of a step)
+    int want_md;          // track max|dU| this step (the last step of a launched sequence)
 };
+
+// fast_step flags: the first step of a launched sequence fills its own face
+// buffer; the last one records max|dU| for the report (solver.cpp:163-167).
+enum StepFlags : int { STEP_FIRST = 1, STEP_LAST = 2 };
 
 inline int axes_stride(int nr, int nv, int ny) { return 5 * nr + 3 * nv + 3 * ny; }
 
@@ -102,7 +108,7 @@ struct LaunchHook {
 void strict_step(const BatchView& v, int s, cudaStream_t stream, long long* launches,
                  const LaunchHook* hook = nullptr);
 void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launches,
-               const LaunchHook* hook = nullptr);
+               const LaunchHook* hook = nullptr, int flags = STEP_FIRST | STEP_LAST);
 // explicit stage alone (stage test of apply_operator / dU0)
 void strict_explicit(const BatchView& v, int s, cudaStream_t stream);
 void fast_explicit(const BatchView& v, int s, cudaStream_t stream);

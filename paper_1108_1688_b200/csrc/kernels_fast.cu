@@ -670,11 +670,8 @@ __device__ __forceinline__ double fval(const BatchView& v, int p, int face, int 
     return __ldg(v.fb + static_cast<size_t>(p) * v.fb_stride + fb_offset(v, face, i, k));
 }
 
-__global__ void __launch_bounds__(256) k_faces(BatchView v, int s) {
-    const int p = blockIdx.y;
-    if (v.st[p].fail_step) return;
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= v.fb_stride) return;
+// entry q of the face buffer of step s (layout as fb_offset)
+__device__ __forceinline__ double face_entry(const BatchView& v, int p, int s, int q) {
     const int nr = v.nr, ny = v.ny;
     int face, i, k;
     if (q < ny) {
@@ -692,10 +689,16 @@ __global__ void __launch_bounds__(256) k_faces(BatchView v, int s) {
         i = t / ny;
         k = t - i * ny;
     }
-    double val = 0.0;
-    if (v.dmask >> face & 1)
-        val = face_value(v.pc[p], step_row(v, p, s), tables(v, p), face, i, k);
-    v.fb[static_cast<size_t>(p) * v.fb_stride + q] = val;
+    if (!(v.dmask >> face & 1)) return 0.0;
+    return face_value(v.pc[p], step_row(v, p, s), tables(v, p), face, i, k);
+}
+
+__global__ void __launch_bounds__(256) k_faces(BatchView v, int s) {
+    const int p = blockIdx.y;
+    if (v.st[p].fail_step) return;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= v.fb_stride) return;
+    v.fb[static_cast<size_t>(p) * v.fb_stride + q] = face_entry(v, p, s, q);
 }
 
 // out-of-line slow paths (take the view by value so the kernels' own copy stays
@@ -1117,8 +1120,9 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const int S = blockDim.y;
     const int nt = 16 * S;
     double* red = sm;                          // [16][S][8] reduced-system rows
-    double* ring = red + nt * 8;               // [kRing][3][nt] window prefetch
-    double* rt = ring + kRing * 3 * nt;        // [nr][8] r-table (FastR)
+    double* ring = red + nt * 8;               // [kRing][4][nt] window prefetch
+    double* rt = ring + kRing * 4 * nt;        // [nr][8] r-table (FastR)
+    double* fy = rt + v.nr * kFR;              // [2][nr] y-face values (YMAX, YMIN)
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
     if (st.fail_step) return;
@@ -1141,6 +1145,10 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const FT F = ftab(v, p);
     for (int e = tid; e < nr * kFR / 2; e += nt)
         reinterpret_cast<double2*>(rt)[e] = __ldg(reinterpret_cast<const double2*>(F.R) + e);
+    {
+        const double* fb0 = v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY;
+        for (int e = tid; e < 2 * nr; e += nt) fy[e] = __ldg(fb0 + e);
+    }
     const double c4 = __ldg(step_row(v, p, s) + ST_C4);
     const double2* V2 = reinterpret_cast<const double2*>(F.V + kFV * j);
     const double2 v01 = __ldg(V2), v23 = __ldg(V2 + 1);  // (V, G2), (G5, G3V)
@@ -1153,7 +1161,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const bool slowj = j == 0 || j == NV - 1;  // block-uniform
     const bool order2y = v.y_order != 1, order2r = v.r_order != 1;
     const double* fbp = v.fb + static_cast<size_t>(p) * v.fb_stride;
-    const double* fby = fbp + 2 * NY + (kN ? 0 : nr);
+    const double* fyk = fy + (kN ? 0 : nr);
     const bool kface = (kN && ymaxD) || (k0 && yminD);
     const double* __restrict__ col = v.U + off + static_cast<size_t>(j) * NY + k;
     double x[M], cs[M], al[M];
@@ -1231,15 +1239,21 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         // window for columns j-1 (0), j (1), j+1 (2): m = row ic-1, c = ic, p = ic+1;
         // rows ic+2 .. ic+1+kRing are in flight in this thread's ring slots
         auto gptr = [&](int ii) { return col + static_cast<size_t>(min(max(ii, 0), nr - 1)) * SR; };
-        auto slot = [&](int q, int c) { return ring + (q * 3 + c) * nt + tid; };
-        double m0, m1, m2, c0, c1, c2, p0, p1, p2;
+        auto slot = [&](int q, int c) { return ring + (q * 4 + c) * nt + tid; };
+        // the 16-lane group's edge lanes also carry their outside neighbour in k
+        // (k-1 at tx 0, k+1 at tx 15; k+2 at k = 0 for the one-sided row)
+        const bool edge = tx == 0 || (tx == 15 && !kN);
+        const int eoff = tx == 0 ? (k0 ? 2 : -1) : 1;
+        double m0, m1, m2, c0, c1, c2, p0, p1, p2, ce = 0.0, pe = 0.0;
         {
             const double* q = gptr(a - 1);
             m0 = __ldg(q - NY); m1 = __ldg(q); m2 = __ldg(q + NY);
             q = gptr(a);
             c0 = __ldg(q - NY); c1 = __ldg(q); c2 = __ldg(q + NY);
+            if (edge) ce = __ldg(q + eoff);
             q = gptr(a + 1);
             p0 = __ldg(q - NY); p1 = __ldg(q); p2 = __ldg(q + NY);
+            if (edge) pe = __ldg(q + eoff);
         }
 #pragma unroll
         for (int q = 0; q < kRing; ++q) {
@@ -1247,6 +1261,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             cp_async8(slot(q, 0), g - NY);
             cp_async8(slot(q, 1), g);
             cp_async8(slot(q, 2), g + NY);
+            if (edge) cp_async8(slot(q, 3), g + eoff);
             cp_async_commit();
         }
         // centre moves to row a+r: row a+r+1 comes out of ring slot (r-1) % kRing,
@@ -1255,35 +1270,34 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             const int q = (r - 1) % kRing;
             cp_async_wait<kRing - 1>();
             m0 = c0; m1 = c1; m2 = c2;
-            c0 = p0; c1 = p1; c2 = p2;
+            c0 = p0; c1 = p1; c2 = p2; ce = pe;
             p0 = *slot(q, 0); p1 = *slot(q, 1); p2 = *slot(q, 2);
+            if (edge) pe = *slot(q, 3);
             const double* g = gptr(a + r + kRing + 1);
             cp_async8(slot(q, 0), g - NY);
             cp_async8(slot(q, 1), g);
             cp_async8(slot(q, 2), g + NY);
+            if (edge) cp_async8(slot(q, 3), g + eoff);
             cp_async_commit();
         };
         // y-direction terms and the k faces (discretization.cpp:340-352)
-        auto yterm = [&](int i, double u0, double acc, double a_i) {
+        auto yterm = [&](int i, double u0, double acc, double a_i, double ed) {
             double kl = __shfl_up_sync(hmask, u0, 1, 16);
             double kr = __shfl_down_sync(hmask, u0, 1, 16);
-            const double* q = col + static_cast<size_t>(i) * SR;
-            if (tx == 0 && !k0) kl = __ldg(q - 1);
-            if (tx == 15 && !kN) kr = __ldg(q + 1);
+            if (tx == 0 && !k0) kl = ed;
+            if (tx == 15 && !kN) kr = ed;
             double yd = kr - kl;
-            if (k0) {  // one-sided y row (discretization.cpp:346-352)
-                const double k2 = __ldg(q + 2);
-                yd = order2y ? fma(4.0, kr, -k2) - 3.0 * u0 : 2.0 * (kr - u0);
-            }
+            if (k0)  // one-sided y row (discretization.cpp:346-352); ed = U(i, j, 2)
+                yd = order2y ? fma(4.0, kr, -ed) - 3.0 * u0 : 2.0 * (kr - u0);
             acc = fma(fma(a_i, vs6, t6), yd, acc);
             double out = acc * dtm;
-            if (kface) out = __ldg(fby + i) - u0;
+            if (kface) out = fyk[i] - u0;
             return out;
         };
         // dU0 at an interior row i from a window (mm, cc, pp)
         auto stencil = [&](int i, const double2& r01, const double2& r45, const double2& r67,
                            double g4h, double mq0, double mq1, double mq2, double cq0, double cq1,
-                           double cq2, double pq0, double pq1, double pq2) {
+                           double cq2, double pq0, double pq1, double pq2, double ed) {
             const double u0 = cq1;
             double acc = -r67.x * u0;
             acc = fma(r01.x * vj, (pq1 + mq1) - 2.0 * u0, acc);
@@ -1291,7 +1305,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             acc = fma(v01.y, (cq2 + cq0) - 2.0 * u0, acc);
             acc = fma(v23.x, cq2 - cq0, acc);
             acc = fma(r45.y * v23.y, (pq2 - pq0) - (mq2 - mq0), acc);
-            return yterm(i, u0, acc, r67.y);
+            return yterm(i, u0, acc, r67.y, ed);
         };
         auto row = [&](int r, double& l, double& d, double& u) {
             const int i = a + r;
@@ -1309,7 +1323,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                     acc = fma(g4h, order2r ? fma(4.0, p1, -n1) - 3.0 * u0 : 2.0 * (p1 - u0), acc);
                     acc = fma(v01.y, (c2 + c0) - 2.0 * u0, acc);
                     acc = fma(v23.x, c2 - c0, acc);
-                    double x0 = yterm(0, u0, acc, r67.y);
+                    double x0 = yterm(0, u0, acc, r67.y, ce);
                     // r_min Dirichlet ranks below r_max / y_max / v_max (discretization.cpp:153-192)
                     if (rminD && !(kN && ymaxD)) x0 = __ldg(fbp + NY + k) - u0;
                     x[0] = x0;
@@ -1317,7 +1331,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                     double2 q01, q23, q45, q67;
                     rtab(1, q01, q23, q45, q67);
                     const double g4h1 = g4(q01, q23, q45);
-                    const double x1 = stencil(1, q01, q45, q67, g4h1, c0, c1, c2, p0, p1, p2, n0, n1, n2);
+                    const double x1 = stencil(1, q01, q45, q67, g4h1, c0, c1, c2, p0, p1, p2, n0, n1, n2, pe);
                     double d0, u0c, s20, l1, d1, u1, t1, l0;
                     coeffs(0, r01.x * vj, g4h, l0, d0, u0c, s20);
                     double f0d = d0, f0u = u0c;
@@ -1333,17 +1347,18 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                             double2 w01, w23, w45, w67;
                             rtab(2, w01, w23, w45, w67);
                             const double x2 = stencil(2, w01, w45, w67, g4(w01, w23, w45), p0, p1, p2, n0,
-                                                      n1, n2, *slot(1, 0), *slot(1, 1), *slot(1, 2));
+                                                      n1, n2, *slot(1, 0), *slot(1, 1), *slot(1, 2),
+                                                      edge ? *slot(0, 3) : 0.0);
                             x[0] = fma(-s20, x2, x[0]);
                         }
                     }
                     l = 0.0; d = f0d; u = f0u;
                     return;
                 }
-                x[0] = stencil(i, r01, r45, r67, g4h, m0, m1, m2, c0, c1, c2, p0, p1, p2);
+                x[0] = stencil(i, r01, r45, r67, g4h, m0, m1, m2, c0, c1, c2, p0, p1, p2, ce);
             } else {
                 shift(r);
-                const double xv = stencil(i, r01, r45, r67, g4h, m0, m1, m2, c0, c1, c2, p0, p1, p2);
+                const double xv = stencil(i, r01, r45, r67, g4h, m0, m1, m2, c0, c1, c2, p0, p1, p2, ce);
                 // face plane i = nr-1: r_max is always Dirichlet and ranks first
                 x[r] = (r == M - 1 && i == nr - 1 && rmaxD) ? __ldg(fbp + k) - c1 : xv;
             }
@@ -1370,12 +1385,19 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         if (r < M - 1) b = -cs[r] * b;
         dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(al[r], left, x[r]));
     }
+    // the face buffer of step s+1 (read from the next step on), spread over the
+    // grid's threads after the march (replaces a k_faces launch per step)
+    if (v.fb_next && s + 1 < v.S) {
+        const int nb = gridDim.x;
+        double* fbn = v.fb_next + static_cast<size_t>(p) * v.fb_stride;
+        for (int e = tid * nb + blockIdx.x; e < v.fb_stride; e += nt * nb) fbn[e] = face_entry(v, p, s + 1, e);
+    }
 }
 
 inline size_t pa_smem(int nr) {
     const int S = nr / 16, nt = 16 * S;
-    return sizeof(double) * (static_cast<size_t>(nt) * 8 + static_cast<size_t>(kRing) * 3 * nt +
-                             static_cast<size_t>(nr) * kFR);
+    return sizeof(double) * (static_cast<size_t>(nt) * 8 + static_cast<size_t>(kRing) * 4 * nt +
+                             static_cast<size_t>(nr) * (kFR + 2));
 }
 
 // ------------------------------------------------------------ pass B, fused plane
@@ -1391,7 +1413,7 @@ inline size_t pa_smem(int nr) {
 // Element (j,k) lives at j*PITCH + (k/16)*17 + k%16: both the column walks
 // (lanes = k) and the segment walks (lanes = segments) are at most 2-way bank
 // conflicted.
-template <int NV, int NY, int CS, int NTX>
+template <int NV, int NY, int CS, int NTX, int MB = 0>
 struct PlaneGeom {
     static constexpr int MS = 16;                 // rows per segment (v and y)
     static constexpr int RV = NV / CS;            // rows j per CTA
@@ -1410,17 +1432,17 @@ struct PlaneGeom {
     static constexpr size_t SMEM = sizeof(double) * (TILE + VT + YT + CAR + EY);
     // CTAs per SM the shared memory allows, capped at 128 registers per thread
     static constexpr int BY_SMEM = static_cast<int>((227 * 1024) / (SMEM + 1024));
-    static constexpr int MINB = (512 / NT) < BY_SMEM ? (512 / NT) : (BY_SMEM > 0 ? BY_SMEM : 1);
+    static constexpr int MINB = MB ? MB : (512 / NT) < BY_SMEM ? (512 / NT) : (BY_SMEM > 0 ? BY_SMEM : 1);
     static_assert(RV % MS == 0 && NY % MS == 0, "segments must tile the plane");
     static_assert(32 % LY == 0 && NT % 32 == 0, "y-lines must not straddle warps");
     static_assert((RV * NY / 2) % NT == 0, "plane rows must split evenly over the block");
     __device__ static int at(int j, int k) { return j * PITCH + (k >> 4) * 17 + (k & 15); }
 };
 
-template <int NV, int NY, int CS, int NTX>
-__global__ void __launch_bounds__(NTX, (PlaneGeom<NV, NY, CS, NTX>::MINB))
+template <int NV, int NY, int CS, int NTX, int MB>
+__global__ void __launch_bounds__(NTX, (PlaneGeom<NV, NY, CS, NTX, MB>::MINB))
 k_plane(BatchView v, int s) {
-    using G = PlaneGeom<NV, NY, CS, NTX>;
+    using G = PlaneGeom<NV, NY, CS, NTX, MB>;
     constexpr int MS = G::MS, LY = G::LY, SV = G::SV, SVL = G::SVL, RV = G::RV, NT = G::NT;
     extern __shared__ double sm[];
     double* tile = sm;
@@ -1573,6 +1595,7 @@ k_plane(BatchView v, int s) {
     const double dint = fma(th, react, 1.0);
     const double bound = pc.bound;
     const double* fby = v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY;  // y faces [nr] x2
+    const bool wmd = v.want_md;
     double md = 0.0;
 #pragma unroll 1
     for (int h = 0; h < G::YROUNDS; ++h) {
@@ -1666,7 +1689,7 @@ k_plane(BatchView v, int s) {
                     dq = fma(b, right, fma(al[r], left, x[r]));
                 }
                 un[r] += dq;
-                md = fmax(md, fabs(dq));
+                if (wmd) md = fmax(md, fabs(dq));
             }
             if (!solve) {
 #pragma unroll
@@ -1676,7 +1699,7 @@ k_plane(BatchView v, int s) {
                 if (sy == LY - 1 && ymaxD) un[MS - 1] = __ldg(fby + i);
             }
 #pragma unroll
-            for (int r = 0; r < MS; ++r)
+            for (int r = 0; r < MS; ++r)  // guard_finite (solver.cpp:69-77)
                 if (!(fabs(un[r]) <= bound))
                     guard_fail(v, p, s, (static_cast<size_t>(i) * NV + j) * NY + a + r, un[r]);
 #pragma unroll
@@ -1690,11 +1713,11 @@ k_plane(BatchView v, int s) {
         atomicMax(&st.maxdelta_bits, static_cast<unsigned long long>(__double_as_longlong(md)));
 }
 
-template <int NV, int NY, int CS, int NT>
+template <int NV, int NY, int CS, int NT, int MB = 0>
 void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
-    using G = PlaneGeom<NV, NY, CS, NT>;
+    using G = PlaneGeom<NV, NY, CS, NT, MB>;
     static const bool attr = [] {
-        cudaFuncSetAttribute(k_plane<NV, NY, CS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_plane<NV, NY, CS, NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(G::SMEM));
         return true;
     }();
@@ -1711,7 +1734,7 @@ void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_plane<NV, NY, CS, NT>, v, s);
+    cudaLaunchKernelEx(&cfg, k_plane<NV, NY, CS, NT, MB>, v, s);
 }
 
 int plane_kernels() {
@@ -1740,8 +1763,18 @@ int fast_stride(int nr, int nv, int ny) { return fast_table_stride(nr, nv, ny); 
 
 void fast_prepare(const BatchView& v, cudaStream_t) { (void)v; }
 
-void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launches,
-               const LaunchHook* hook) {
+void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launches,
+               const LaunchHook* hook, int flags) {
+    // face buffers alternate by step parity: kernels of step s read w.fb, the
+    // plane kernel (last of the step) fills w.fb_next for step s+1
+    BatchView w = v0;
+    if (w.fb) {
+        const size_t half = static_cast<size_t>(w.P) * w.fb_stride;
+        w.fb = v0.fb + (s & 1) * half;
+        w.fb_next = v0.fb + ((s + 1) & 1) * half;
+    }
+    w.want_md = (flags & STEP_LAST) ? 1 : 0;
+    const BatchView& v = w;
     auto mark = [&](int idx, const char* name, double bytes) {
         if (launches) ++*launches;
         if (hook && hook->after) hook->after(hook->ctx, idx, name, bytes);
@@ -1750,13 +1783,26 @@ void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launch
     // write dU0 | read + write the line | read + write the line | read dU, read U, write U
     const int tk = (v.ny + 31) / 32, tj = (v.nv + 7) / 8;
     const int shape = specialised_shape(v);
-    k_faces<<<dim3((v.fb_stride + 255) / 256, v.P), 256, 0, stream>>>(v, s);
-    mark(4, "fx_faces", 0.0);
+    const int pl = plane_kernels();
+    const bool plane = pl && (shape == 32 || shape == 64 || shape == 128 || (shape == 256 && pl == 3));
     static const int pa_env = [] {
         const char* e = std::getenv("HJMSV_PA");
         return e ? std::atoi(e) : 1;
     }();
-    if (pa_env && shape != 0 && v.nr % 16 == 0 && v.nr / 16 <= 32) {
+    const bool pa = pa_env && shape != 0 && v.nr % 16 == 0 && v.nr / 16 <= 32;
+    // folding the face table into pass A pays off for single grids; a large
+    // batch computes it faster as its own full-occupancy launch (measured)
+    static const int fold_env = [] {
+        const char* e = std::getenv("HJMSV_FOLD");
+        return e ? std::atoi(e) : -1;
+    }();
+    const bool fold = pa && (fold_env < 0 ? v.P <= 8 : fold_env > 0);
+    if (!fold) w.fb_next = nullptr;
+    if (!fold || (flags & STEP_FIRST)) {  // otherwise pass A of step s-1 filled it
+        k_faces<<<dim3((v.fb_stride + 255) / 256, v.P), 256, 0, stream>>>(v, s);
+        mark(4, "fx_faces", 0.0);
+    }
+    if (pa) {
         // pass A fused: explicit stencil + r-lines
         const int S = v.nr / 16;
         const dim3 g(v.nv * (v.ny / 16), v.P), b(16, S);
@@ -1792,13 +1838,15 @@ void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launch
                         static_cast<size_t>(kLanesR) * Sr * 8 * sizeof(double), stream>>>(v, s);
         mark(1, "fx_sweep_r", 16.0);
     }
-    const int pl = plane_kernels();
-    if (pl && (shape == 32 || shape == 64 || shape == 128 || (shape == 256 && pl == 3))) {
+    if (plane) {
         // pass B fused: v-lines + y-lines + update on an SMEM-resident plane
         if (shape == 32) launch_plane<32, 32, 1, 64>(v, s, stream);
         else if (shape == 64) launch_plane<64, 64, 1, 256>(v, s, stream);
         else if (shape == 128) {
             if (pl == 3) launch_plane<128, 128, 2, 256>(v, s, stream);
+            else if (pl == 4) launch_plane<128, 128, 2, 128, 2>(v, s, stream);
+            else if (pl == 5) launch_plane<128, 128, 4, 128, 2>(v, s, stream);
+            else if (pl == 6) launch_plane<128, 128, 2, 256, 1>(v, s, stream);
             else launch_plane<128, 128, 1, 256>(v, s, stream);
         } else launch_plane<256, 256, 8, 256>(v, s, stream);
         mark(2, "fx_plane_vy_update", 24.0);
