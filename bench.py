@@ -211,6 +211,18 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
+    (profiles/ncu_traffic.json), or None if that kernel was not captured."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            ent = json.load(f).get(kernel)
+        return float(ent["dram_bytes"]) if ent else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -275,12 +287,12 @@ def main():
     # live per-kernel roofline: dominant kernel of one march
     solver.reset()
     prof, _ = solver.kernel_profile(solver.n_steps)
-    march_ms = sum(k["avg_ms"] * solver.n_steps for k in prof) or 1.0
+    march_ms = ms_per_step or 1.0  # the measured march (one bench step) on this rank
     dom = max(prof, key=lambda k: k["avg_ms"])
     peak, peak_kind = measured_peak()
     achieved = dom["alg_bytes"] / (dom["avg_ms"] / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "kernel": dom["name"],
+                "frac": achieved / peak, "traffic": ncu_traffic(dom["name"]), "kernel": dom["name"],
                 "kernel_share_of_step": dom["avg_ms"] * solver.n_steps / march_ms,
                 "peak_kind": peak_kind,
                 "step_equiv_GBps": total_pts * args.steps * 40.0 / (total_ms / 1e3) / 1e9 / world,

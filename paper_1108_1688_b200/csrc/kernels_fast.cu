@@ -247,37 +247,38 @@ __device__ __forceinline__ bool seg_solve(int m, double (&x)[M], double (&cs)[M]
 // Forward: q_t = Qc_t + Qd_t q_{t+1}, p_t = Pp_t + Pq_t q_{t+1}; backward from
 // q_{S-1} = 0. Segment t's data at E[t*stride + f] (f: yF aF bF yL aL bL); the
 // results p_t, q_t overwrite fields 6, 7.
-__device__ __forceinline__ bool reduced_solve(double* E, int S, int stride, int& bad_t) {
+__device__ __forceinline__ bool reduced_solve(double* E, int S, int stride, int& bad_t, int fs = 1) {
+    // element (t, f) at E[t*stride + f*fs]
     double Pp = 0.0, Pq = 0.0;
     bool ok = true;
 #pragma unroll 1
     for (int t = 0; t < S - 1; ++t) {
         double* e0 = E + t * stride;
         const double* e1 = e0 + stride;
-        const double A = fma(e0[4], Pp, e0[3]);
-        const double B = fma(e0[4], Pq, e0[5]);
-        const double den = fma(-e1[1], B, 1.0);
+        const double A = fma(e0[4 * fs], Pp, e0[3 * fs]);
+        const double B = fma(e0[4 * fs], Pq, e0[5 * fs]);
+        const double den = fma(-e1[1 * fs], B, 1.0);
         if (fabs(den) < 1e-300 && ok) {
             ok = false;
             bad_t = t + 1;
         }
         const double inv = frcp(den);
-        const double Qc = fma(e1[1], A, e1[0]) * inv;
-        const double Qd = e1[2] * inv;
+        const double Qc = fma(e1[1 * fs], A, e1[0]) * inv;
+        const double Qd = e1[2 * fs] * inv;
         Pp = fma(B, Qc, A);
         Pq = B * Qd;
-        e0[6] = Qc;
-        e0[7] = Qd;
-        e0[3] = Pp;
-        e0[4] = Pq;
+        e0[6 * fs] = Qc;
+        e0[7 * fs] = Qd;
+        e0[3 * fs] = Pp;
+        e0[4 * fs] = Pq;
     }
     double qn = 0.0;
 #pragma unroll 1
     for (int t = S - 2; t >= 0; --t) {
         double* e0 = E + t * stride;
-        const double qs = fma(e0[7], qn, e0[6]);
-        e0[6] = fma(e0[4], qn, e0[3]);  // p_t
-        e0[7] = qs;                     // q_t
+        const double qs = fma(e0[7 * fs], qn, e0[6 * fs]);
+        e0[6 * fs] = fma(e0[4 * fs], qn, e0[3 * fs]);  // p_t
+        e0[7 * fs] = qs;                               // q_t
         qn = qs;
     }
     return ok;
@@ -1108,6 +1109,10 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -1125,14 +1130,13 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     double* fy = rt + v.nr * kFR;              // [2][nr] y-face values (YMAX, YMIN)
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
-    if (st.fail_step) return;
+    const int fail = st.fail_step;  // checked after the prologue loads are in flight
     const int nr = v.nr;
     const int tx = threadIdx.x, sg = threadIdx.y;
     const int tid = sg * 16 + tx;
     constexpr int TK = NY / 16;
     const int j = blockIdx.x / TK;
     const int k = (blockIdx.x - j * TK) * 16 + tx;
-    if (blockIdx.x == 0 && tid == 0) st.maxdelta_bits = 0ull;
     const ProblemConst& pc = v.pc[p];
     const bool yminD = dir(v, F_YMIN), ymaxD = dir(v, F_YMAX);
     const bool k0 = k == 0, kN = k == NY - 1;
@@ -1143,12 +1147,14 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const int a = sg * M;
     const size_t off = static_cast<size_t>(p) * v.N;
     const FT F = ftab(v, p);
-    for (int e = tid; e < nr * kFR / 2; e += nt)
-        reinterpret_cast<double2*>(rt)[e] = __ldg(reinterpret_cast<const double2*>(F.R) + e);
+    // r-table and y-face values into shared memory asynchronously (group 0),
+    // overlapped with the window prologue below
+    for (int e = tid; e < nr * kFR / 2; e += nt) cp_async16(rt + 2 * e, F.R + 2 * e);
     {
         const double* fb0 = v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY;
-        for (int e = tid; e < 2 * nr; e += nt) fy[e] = __ldg(fb0 + e);
+        for (int e = tid; e < 2 * nr; e += nt) cp_async8(fy + e, fb0 + e);
     }
+    cp_async_commit();
     const double c4 = __ldg(step_row(v, p, s) + ST_C4);
     const double2* V2 = reinterpret_cast<const double2*>(F.V + kFV * j);
     const double2 v01 = __ldg(V2), v23 = __ldg(V2 + 1);  // (V, G2), (G5, G3V)
@@ -1165,7 +1171,43 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const bool kface = (kN && ymaxD) || (k0 && yminD);
     const double* __restrict__ col = v.U + off + static_cast<size_t>(j) * NY + k;
     double x[M], cs[M], al[M];
-    __syncthreads();  // rt
+    // window for columns j-1 (0), j (1), j+1 (2): m = row ic-1, c = ic, p = ic+1;
+    // rows ic+2 .. ic+1+kRing are in flight in this thread's ring slots (groups 1..kRing)
+    double m0 = 0.0, m1 = 0.0, m2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, p0 = 0.0, p1 = 0.0, p2 = 0.0;
+    double ce = 0.0, pe = 0.0;
+    auto gptr = [&](int ii) { return col + static_cast<size_t>(min(max(ii, 0), nr - 1)) * SR; };
+    auto slot = [&](int q, int c) { return ring + (q * 4 + c) * nt + tid; };
+    // the 16-lane group's edge lanes also carry their outside neighbour in k
+    // (k-1 at tx 0, k+1 at tx 15; k+2 at k = 0 for the one-sided row)
+    const bool edge = tx == 0 || (tx == 15 && !kN);
+    const int eoff = tx == 0 ? (k0 ? 2 : -1) : 1;
+    if (!slowj) {
+        const double* q = gptr(a - 1);
+        m0 = __ldg(q - NY); m1 = __ldg(q); m2 = __ldg(q + NY);
+        q = gptr(a);
+        c0 = __ldg(q - NY); c1 = __ldg(q); c2 = __ldg(q + NY);
+        if (edge) ce = __ldg(q + eoff);
+        q = gptr(a + 1);
+        p0 = __ldg(q - NY); p1 = __ldg(q); p2 = __ldg(q + NY);
+        if (edge) pe = __ldg(q + eoff);
+#pragma unroll
+        for (int r = 0; r < kRing; ++r) {
+            const double* g = gptr(a + 2 + r);
+            cp_async8(slot(r, 0), g - NY);
+            cp_async8(slot(r, 1), g);
+            cp_async8(slot(r, 2), g + NY);
+            if (edge) cp_async8(slot(r, 3), g + eoff);
+            cp_async_commit();
+        }
+    }
+    if (fail) {  // the problem failed in an earlier step (block-uniform)
+        cp_async_wait<0>();
+        return;
+    }
+    if (blockIdx.x == 0 && tid == 0) st.maxdelta_bits = 0ull;
+    if (slowj) cp_async_wait<0>();
+    else cp_async_wait<kRing>();  // group 0 (tables) done; the ring may still be in flight
+    __syncthreads();  // rt, fy
 
     // row coefficients of I - th L_r at row i (g4h shared with the stencil)
     auto coeffs = [&](int i, double g1s, double g4h, double& l, double& d, double& u, double& s2) {
@@ -1238,32 +1280,6 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     } else {
         // window for columns j-1 (0), j (1), j+1 (2): m = row ic-1, c = ic, p = ic+1;
         // rows ic+2 .. ic+1+kRing are in flight in this thread's ring slots
-        auto gptr = [&](int ii) { return col + static_cast<size_t>(min(max(ii, 0), nr - 1)) * SR; };
-        auto slot = [&](int q, int c) { return ring + (q * 4 + c) * nt + tid; };
-        // the 16-lane group's edge lanes also carry their outside neighbour in k
-        // (k-1 at tx 0, k+1 at tx 15; k+2 at k = 0 for the one-sided row)
-        const bool edge = tx == 0 || (tx == 15 && !kN);
-        const int eoff = tx == 0 ? (k0 ? 2 : -1) : 1;
-        double m0, m1, m2, c0, c1, c2, p0, p1, p2, ce = 0.0, pe = 0.0;
-        {
-            const double* q = gptr(a - 1);
-            m0 = __ldg(q - NY); m1 = __ldg(q); m2 = __ldg(q + NY);
-            q = gptr(a);
-            c0 = __ldg(q - NY); c1 = __ldg(q); c2 = __ldg(q + NY);
-            if (edge) ce = __ldg(q + eoff);
-            q = gptr(a + 1);
-            p0 = __ldg(q - NY); p1 = __ldg(q); p2 = __ldg(q + NY);
-            if (edge) pe = __ldg(q + eoff);
-        }
-#pragma unroll
-        for (int q = 0; q < kRing; ++q) {
-            const double* g = gptr(a + 2 + q);
-            cp_async8(slot(q, 0), g - NY);
-            cp_async8(slot(q, 1), g);
-            cp_async8(slot(q, 2), g + NY);
-            if (edge) cp_async8(slot(q, 3), g + eoff);
-            cp_async_commit();
-        }
         // centre moves to row a+r: row a+r+1 comes out of ring slot (r-1) % kRing,
         // which is refilled with row a+r+kRing+1
         auto shift = [&](int r) {
@@ -1368,16 +1384,18 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         cp_async_wait<0>();
     }
     if (!ok) record_pivot(st, s, 0, j * NY + k, a + bad_r);
-    double* E = red + (tx * S + sg) * 8;
-    E[0] = yF; E[1] = aF; E[2] = bF; E[3] = yL; E[4] = aL; E[5] = bL;
+    // reduced-system rows as [segment][field][lane]: the column walks of the
+    // reduced solve (lanes = k) are bank-conflict free
+    double* E = red + sg * 8 * 16 + tx;
+    E[0] = yF; E[16] = aF; E[32] = bF; E[48] = yL; E[64] = aL; E[80] = bL;
     __syncthreads();
     if (sg == 0 && solve && S > 1) {
         int bt = 0;
-        if (!reduced_solve(red + tx * S * 8, S, 8, bt)) record_pivot(st, s, 0, j * NY + k, bt * M);
+        if (!reduced_solve(red + tx, S, 8 * 16, bt, 16)) record_pivot(st, s, 0, j * NY + k, bt * M);
     }
     __syncthreads();
-    const double left = (solve && sg > 0) ? E[-8 + 6] : 0.0;  // p_{s-1} = x_{a-1}
-    const double right = (solve && sg < S - 1) ? E[7] : 0.0;  // q_s = x_{a+m}
+    const double left = (solve && sg > 0) ? E[-8 * 16 + 6 * 16] : 0.0;  // p_{s-1} = x_{a-1}
+    const double right = (solve && sg < S - 1) ? E[7 * 16] : 0.0;        // q_s = x_{a+m}
     double b = bL;
     double* __restrict__ dcol = v.D + off + static_cast<size_t>(j) * NY + k + static_cast<size_t>(a) * SR;
 #pragma unroll
@@ -1428,7 +1446,7 @@ struct PlaneGeom {
     static constexpr int VT = 5 * NV;             // v tables: RP B E BF BB
     static constexpr int YT = 2 * (LY * 17);      // y tables: (S6, T6) pairs, 17-pair segments
     static constexpr int CAR = 2 * SV * NY;       // v carries (all segments, both directions)
-    static constexpr int EY = NT * 8;             // y reduced-system rows per round
+    static constexpr int EY = (NT / 32) * ((NY / 16) * (8 * (32 / (NY / 16)) + 1) + 1);  // per warp: LY x TS + 1
     static constexpr size_t SMEM = sizeof(double) * (TILE + VT + YT + CAR + EY);
     // CTAs per SM the shared memory allows, capped at 128 registers per thread
     static constexpr int BY_SMEM = static_cast<int>((227 * 1024) / (SMEM + 1024));
@@ -1474,7 +1492,7 @@ k_plane(BatchView v, int s) {
     const size_t off = static_cast<size_t>(p) * v.N;
     const size_t pb = off + (static_cast<size_t>(i) * NV + j0) * NY;  // first row of this CTA
     const FT F = ftab(v, p);
-    if (live_p) {
+    {  // staged even for a failed problem: the loads need not wait for the status word
         if (tid == 0) {  // U rows -> L2 early, so the update's loads hit L2
             constexpr unsigned bytes = RV * NY * sizeof(double);
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.U + pb), "r"(bytes) : "memory");
@@ -1658,20 +1676,23 @@ k_plane(BatchView v, int s) {
             if (!seg_solve<MS>(MS, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row))
                 record_pivot(st, s, 2, i * NV + j, a + bad_r);
         }
-        const int lslot = (tid / LY) * LY * 8 + sy * 8;  // line-local slot in ey
+        // reduced-system rows of the warp's lines as [segment][field][line] (padded),
+        // so the per-line reduced solves (lanes = lines) are bank-conflict free
+        constexpr int LPW = 32 / LY, TS = 8 * LPW + 1;
+        double* ew = ey + (tid >> 5) * (LY * TS + 1) + (tid & 31) / LY;  // this line's (0, 0)
+        double* e = ew + sy * TS;
         if (live) {
-            double* e = ey + lslot;
-            e[0] = yF; e[1] = aF; e[2] = bF; e[3] = yL; e[4] = aL; e[5] = bL;
+            e[0] = yF; e[LPW] = aF; e[2 * LPW] = bF; e[3 * LPW] = yL; e[4 * LPW] = aL; e[5 * LPW] = bL;
         }
         __syncwarp();  // a line's LY segments lie in one warp
         if (solve && sy == 0 && LY > 1) {
             int bt = 0;
-            if (!reduced_solve(ey + lslot, LY, 8, bt)) record_pivot(st, s, 2, i * NV + j, bt * MS);
+            if (!reduced_solve(ew, LY, TS, bt, LPW)) record_pivot(st, s, 2, i * NV + j, bt * MS);
         }
         __syncwarp();
         if (live) {
-            const double left = (solve && sy > 0) ? ey[lslot - 8 + 6] : 0.0;
-            const double right = (solve && sy < LY - 1) ? ey[lslot + 7] : 0.0;
+            const double left = (solve && sy > 0) ? e[-TS + 6 * LPW] : 0.0;
+            const double right = (solve && sy < LY - 1) ? e[7 * LPW] : 0.0;
             double* up = v.U + pb + static_cast<size_t>(jl) * NY + a;
             double un[MS];
 #pragma unroll

@@ -32,6 +32,7 @@ def num(r, h):
 tot_i = sum(num(r, "Instructions Executed") for _, r in rows) or 1
 tot_s = sum(num(r, "# Samples") for _, r in rows) or 1
 print(f"warp-instructions={tot_i:.0f} samples={tot_s:.0f}")
-for f, r in sorted(rows, key=lambda x: -num(x[1], "Instructions Executed"))[:N]:
+key = "# Samples" if len(sys.argv) > 4 else "Instructions Executed"
+for f, r in sorted(rows, key=lambda x: -num(x[1], key))[:N]:
     print(f"{f}:{r[0]:>5} inst={100 * num(r, 'Instructions Executed') / tot_i:5.1f}% "
           f"samp={100 * num(r, '# Samples') / tot_s:5.1f}% | {r[1].strip()[:90]}")
