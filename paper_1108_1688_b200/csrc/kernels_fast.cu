@@ -1684,6 +1684,16 @@ k_plane(BatchView v, int s) {
         if (live) {
             e[0] = yF; e[LPW] = aF; e[2 * LPW] = bF; e[3 * LPW] = yL; e[4 * LPW] = aL; e[5 * LPW] = bL;
         }
+        double* up = v.U + pb + static_cast<size_t>(jl) * NY + a;
+        double un[MS];
+        auto load_u = [&] {
+#pragma unroll
+            for (int q = 0; q < MS / 2; ++q) {
+                const double2 t = reinterpret_cast<const double2*>(up)[q];
+                un[2 * q] = t.x;
+                un[2 * q + 1] = t.y;
+            }
+        };
         __syncwarp();  // a line's LY segments lie in one warp
         if (solve && sy == 0 && LY > 1) {
             int bt = 0;
@@ -1693,14 +1703,7 @@ k_plane(BatchView v, int s) {
         if (live) {
             const double left = (solve && sy > 0) ? e[-TS + 6 * LPW] : 0.0;
             const double right = (solve && sy < LY - 1) ? e[7 * LPW] : 0.0;
-            double* up = v.U + pb + static_cast<size_t>(jl) * NY + a;
-            double un[MS];
-#pragma unroll
-            for (int q = 0; q < MS / 2; ++q) {
-                const double2 t = reinterpret_cast<const double2*>(up)[q];
-                un[2 * q] = t.x;
-                un[2 * q + 1] = t.y;
-            }
+            load_u();
             double b = bL;
 #pragma unroll
             for (int r = MS - 1; r >= 0; --r) {
@@ -1710,7 +1713,11 @@ k_plane(BatchView v, int s) {
                     dq = fma(b, right, fma(al[r], left, x[r]));
                 }
                 un[r] += dq;
-                if (wmd) md = fmax(md, fabs(dq));
+                x[r] = dq;
+            }
+            if (wmd) {
+#pragma unroll
+                for (int r = 0; r < MS; ++r) md = fmax(md, fabs(x[r]));
             }
             if (!solve) {
 #pragma unroll
