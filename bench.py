@@ -336,11 +336,19 @@ def main():
         el = torch.tensor([sum(e2e_t)], dtype=torch.float64, device="cuda")
         if dist:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
-        h2d = sum(8 * p.size + 8 * (p.r.n + p.v.n + p.y.n) * 3 + 8 * 32 * p.n_steps for p in probs)
+        # descriptor tables per problem: axes, per-step scalars, FAST factor tables,
+        # constants, readout corners; the terminal level is built on the device in
+        # FAST mode and uploaded only in STRICT mode
+        def h2d_bytes(p):
+            nr, nv, ny = p.r.n, p.v.n, p.y.n
+            b = 8 * (5 * nr + 3 * nv + 3 * ny) + 8 * 32 * p.n_steps + 256 + 8 * 16 + 48
+            b += 8 * (8 * nr + 10 * nv + 4 * ny) if args.mode == "fast" else 8 * p.size
+            return b
+        h2d = sum(h2d_bytes(p) for p in probs)
         d2h = sum(8 * p.size for p in probs) + 8 * len(probs)
         e2e = {"value": total_pts * reps / float(el[0]), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "note": "per step: create(lower+terminal+H2D) -> run -> spot prices + grid D2H -> destroy"}
+               "note": "per step: create(lower + descriptor H2D + device terminal) -> run -> spot prices + grid D2H -> destroy"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

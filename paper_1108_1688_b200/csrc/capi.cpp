@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -207,8 +208,35 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
     if (mode != HJMSV_MODE_STRICT && mode != HJMSV_MODE_FAST)
         throw std::invalid_argument("unknown arithmetic mode");
     std::vector<Lowered> L(count);
+    // FAST marches build the terminal level on the device;
+    // STRICT keeps the host restatement, bit-identical to smooth_terminal
+    const int init_mode = (mode == HJMSV_MODE_FAST && !ov) ? INIT_DEVICE : INIT_HOST;
+    {
+        // lower the problems on all host cores (each lowering is independent)
+        std::vector<std::exception_ptr> errs(count);
+        auto one = [&](int p) {
+            try {
+                L[p] = lower_problem(problems[p], cfg, init_mode);
+            } catch (...) {
+                errs[p] = std::current_exception();
+            }
+        };
+        const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+        const int workers = init_mode == INIT_DEVICE ? std::min(hw, count) : 1;
+        if (workers <= 1) {
+            for (int p = 0; p < count; ++p) one(p);
+        } else {
+            std::vector<std::thread> pool;
+            for (int w = 0; w < workers; ++w)
+                pool.emplace_back([&, w] {
+                    for (int p = w; p < count; p += workers) one(p);
+                });
+            for (auto& t : pool) t.join();
+        }
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);  // the first problem's error, in input order
+    }
     for (int p = 0; p < count; ++p) {
-        L[p] = lower_problem(problems[p], cfg, true);
         if (ov) {  // one explicit level (t_from, dt): the douglas_step / apply_operator stages
             L[p].n_steps = 1;
             L[p].dt = ov->dt;
@@ -255,14 +283,20 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
     h->spot_idx_host.resize(static_cast<size_t>(count) * 8);
     h->spot_w_host.resize(static_cast<size_t>(count) * 8);
     h->term_steps.resize(count);
+    std::vector<double> axes_h(static_cast<size_t>(count) * astride);
+    std::vector<double> steps_h(static_cast<size_t>(count) * h->S * kStepStride);
+    std::vector<TermParam> term_h(count);
+    std::vector<int> term_kind(count);
     for (int p = 0; p < count; ++p) {
         const Lowered& l = L[p];
-        CK(cudaMemcpy(h->U0 + static_cast<size_t>(p) * h->N, l.init.data(),
-                      sizeof(double) * h->N, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->axes + static_cast<size_t>(p) * astride, l.axes.data(),
-                      sizeof(double) * astride, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->steps + static_cast<size_t>(p) * h->S * kStepStride, l.steps.data(),
-                      sizeof(double) * l.steps.size(), cudaMemcpyHostToDevice));
+        term_h[p] = l.term;
+        term_kind[p] = l.term.kind;
+        if (l.term.kind == TERM_HOST)
+            CK(cudaMemcpy(h->U0 + static_cast<size_t>(p) * h->N, l.init.data(),
+                          sizeof(double) * h->N, cudaMemcpyHostToDevice));
+        std::copy(l.axes.begin(), l.axes.end(), axes_h.begin() + static_cast<size_t>(p) * astride);
+        std::copy(l.steps.begin(), l.steps.end(),
+                  steps_h.begin() + static_cast<size_t>(p) * h->S * kStepStride);
         pcs[p] = l.pc;
         std::copy(l.spot_idx, l.spot_idx + 8, h->spot_idx_host.begin() + p * 8);
         std::copy(l.spot_w, l.spot_w + 8, h->spot_w_host.begin() + p * 8);
@@ -271,6 +305,8 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         for (int s = 0; s < h->S; ++s)
             h->term_steps[p].push_back(l.steps[static_cast<size_t>(s) * kStepStride + ST_TNEXT]);
     }
+    CK(cudaMemcpy(h->axes, axes_h.data(), sizeof(double) * axes_h.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->steps, steps_h.data(), sizeof(double) * steps_h.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->pc, pcs.data(), sizeof(ProblemConst) * count, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->spot_idx, h->spot_idx_host.data(), sizeof(long long) * 8 * count,
                   cudaMemcpyHostToDevice));
@@ -313,12 +349,20 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         v.fb_stride = 2 * h->ny + 2 * h->nr + 2 * h->nr * h->ny;
         h->fb = dalloc<double>(2 * static_cast<size_t>(count) * v.fb_stride);  // two step parities
         v.fb = h->fb;
+        std::vector<double> fast_h(static_cast<size_t>(count) * v.fast_stride);
         for (int p = 0; p < count; ++p) {
             const std::vector<double> ft = build_fast_tables(L[p], cfg, L[p].pc.theta_dt);
-            CK(cudaMemcpy(h->fast + static_cast<size_t>(p) * v.fast_stride, ft.data(),
-                          sizeof(double) * ft.size(), cudaMemcpyHostToDevice));
+            std::copy(ft.begin(), ft.end(), fast_h.begin() + static_cast<size_t>(p) * v.fast_stride);
         }
+        CK(cudaMemcpy(h->fast, fast_h.data(), sizeof(double) * fast_h.size(), cudaMemcpyHostToDevice));
         fast_prepare(v, h->stream);
+    }
+    if (init_mode == INIT_DEVICE) {
+        TermParam* tp = dalloc<TermParam>(count);
+        CK(cudaMemcpy(tp, term_h.data(), sizeof(TermParam) * count, cudaMemcpyHostToDevice));
+        device_terminal(v, tp, term_kind.data(), h->U0, h->stream);
+        CK(cudaStreamSynchronize(h->stream));
+        dfree(tp);
     }
     h->reports.assign(count, hjmsv_report{});
     h->messages.assign(count, std::string());

@@ -97,6 +97,20 @@ enum FastY : int { FY_S6 = 0, FY_T6, FY_Y, FY_PAD };
 constexpr int kSegV = 16;  // rows per segment of the segmented v-solve
 inline int fast_table_stride(int nr, int nv, int ny) { return kFR * nr + kFV * nv + kFY * ny; }
 
+// Terminal level built on the device (FAST mode): ZCB = 1 everywhere; caplet =
+// caplet_payoff (model.cpp:105-112) with smooth_terminal's cell averages
+// (solver.cpp:180-211), from per-problem scalars of the host curve.
+enum TermKind : int { TERM_HOST = 0, TERM_ONES = 1, TERM_CAPLET = 2 };
+struct TermParam {
+    int kind;
+    int m;            // samples per axis (1 without smoothing)
+    double r0;
+    double f_t;       // f(0, T)
+    double accrual;   // 1 + (T_M - T) K (model.hpp:55)
+    double ratio;     // p(0, T_M) / p(0, T)
+    double g;         // g_factor(T_M - T, kappa)
+};
+
 // Per-kernel hook for the live profiler: called after each launch with the
 // kernel's index, name and ALGORITHMIC bytes per grid point of that launch.
 struct LaunchHook {
@@ -116,6 +130,9 @@ void fast_prepare(const BatchView& v, cudaStream_t stream);  // builds v.fast fr
 int fast_stride(int nr, int nv, int ny);
 bool fast_supported(int nr, int nv, int ny);
 void reset_status(const BatchView& v, cudaStream_t stream);
+// U0[p] = terminal level of problem p for every p with tp[p].kind != TERM_HOST
+void device_terminal(const BatchView& v, const TermParam* tp, const int* host_kinds, double* U0,
+                     cudaStream_t stream);
 // trilinear readout: out[p] = sum_q w[p*8+q] * U[p][idx[p*8+q]] (instruments.cpp:71-88)
 void gather_spot(const BatchView& v, const long long* idx, const double* w, double* out,
                  cudaStream_t stream);

@@ -226,7 +226,7 @@ void locate_point(const Lowered& L, double zr, double zv, double zy, long long i
             }
 }
 
-Lowered lower_problem(const hjmsv_problem& p, const hjmsv_solver_config& cfg, bool build_init) {
+Lowered lower_problem(const hjmsv_problem& p, const hjmsv_solver_config& cfg, int init_mode) {
     validate_config(cfg);
     if (p.maturity <= 0.0) throw std::invalid_argument("run: maturity must be positive");
     if (p.instrument == HJMSV_INSTRUMENT_CAPLET) {  // CapletSpec::validate, model.cpp:35-39
@@ -335,7 +335,21 @@ Lowered lower_problem(const hjmsv_problem& p, const hjmsv_solver_config& cfg, bo
     const double f0 = L.curve.forward(0.0);
     locate_point(L, f0 / p.r0, 1.0, 0.0 / (p.r0 * p.r0), L.spot_idx, L.spot_w);
 
-    if (build_init) {
+    if (init_mode == INIT_DEVICE && !p.initial_grid &&
+        (p.instrument == HJMSV_INSTRUMENT_ZCB || p.instrument == HJMSV_INSTRUMENT_CAPLET)) {
+        TermParam& tp = L.term;
+        tp.m = cfg.smoothing ? cfg.smoothing_subsamples : 1;
+        tp.r0 = p.r0;
+        if (p.instrument == HJMSV_INSTRUMENT_ZCB) {
+            tp.kind = TERM_ONES;
+        } else {  // the scalars caplet_terminal's payoff closes over
+            tp.kind = TERM_CAPLET;
+            tp.f_t = L.curve.forward(p.maturity);
+            tp.accrual = 1.0 + (p.payment - p.maturity) * p.strike;
+            tp.ratio = L.curve.discount(p.payment) / L.curve.discount(p.maturity);
+            tp.g = g_factor(p.payment - p.maturity, p.model.kappa);
+        }
+    } else if (init_mode != INIT_NONE) {
         const size_t N = static_cast<size_t>(nr) * nv * ny;
         if (p.initial_grid) {
             L.init.assign(p.initial_grid, p.initial_grid + N);

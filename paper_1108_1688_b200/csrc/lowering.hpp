@@ -23,14 +23,20 @@ struct Lowered {
     double term_t[kMaxTerms] = {};  // maturity of each closed-form term slot
     long long spot_idx[8] = {};  // interpolate_at corners at natural_spot
     double spot_w[8] = {};
+    TermParam term{};            // terminal built on the device (kind != TERM_HOST)
 };
+
+/// How lower_problem provides the terminal level: on the host (L.init) or as
+/// device terminal parameters (L.term) for ZCB / caplet problems without an
+/// explicit initial grid (smooth_terminal + caplet_payoff, solver.cpp:180-211).
+enum InitMode { INIT_NONE = 0, INIT_HOST = 1, INIT_DEVICE = 2 };
 
 /// Validates exactly like run() (solver.cpp:214-216), SolverConfig::validate
 /// (solver.cpp:10-20), ModelParams::validate (model.cpp:25-33), CapletSpec::validate
 /// (model.cpp:35-39), HjmCoefficientField (discretization.cpp:34-35) and
 /// SpatialOperator (discretization.cpp:144-150), then builds every table.
 /// Throws the reference's exception types/messages.
-Lowered lower_problem(const hjmsv_problem& p, const hjmsv_solver_config& cfg, bool build_init);
+Lowered lower_problem(const hjmsv_problem& p, const hjmsv_solver_config& cfg, int init_mode);
 
 /// Per-step scalar table for explicit (t_from, dt) levels; used by the march
 /// (time levels of run() or the indexed harness) and by the single-step stage.

@@ -203,3 +203,24 @@ def test_batch_run_driver(gpu, oracle):
         assert B.normwise_rel(g, g_ref) <= STRICT_TOL
         assert abs(prices[q] - oracle.spot_price(p, g_ref)) <= TOL * abs(prices[q])
         assert reps[q]["status"] == 0
+
+
+@pytest.mark.parametrize("smoothing", [True, False])
+def test_device_terminal_matches_host(gpu, oracle, smoothing):
+    """FAST builds the terminal level on the device (smooth_terminal,
+    solver.cpp:180-211, caplet_payoff model.cpp:105-112); it must match the host
+    restatement up to libm-vs-device exp ulps, for caplets on uniform and sinh meshes."""
+    cfg = hj.SolverConfig(smoothing=smoothing)
+    probs = W.make_config(2, count=3, nr=32, nv=16, ny=16, steps=10)
+    sinh = W.make_problem(2, 5, nr=24, nv=12, ny=20, steps=10)
+    sinh.r = AxisSpec.sinh(sinh.strike / sinh.r0, 0.05, 0.0, 250.0, 24)
+    sinh.v = AxisSpec.sinh(0.5, 0.5, 0.0, 30.0, 12)
+    sinh.y = AxisSpec.sinh(0.0, 0.05, 0.0, 250.0, 20)
+    zcb = W.make_problem(0, 0, nr=16, nv=8, ny=8, steps=10)
+    for batch in (probs, [sinh], [zcb]):
+        with hj.Solver(batch, mode="fast", config=cfg) as s:
+            for q, p in enumerate(batch):
+                ref = oracle.initial_level(p, cfg)
+                g = s.grid(q)
+                err = np.max(np.abs(g - ref)) / max(np.max(np.abs(ref)), 1e-300)
+                assert err <= 1e-14, f"terminal max rel err {err:.3e}"
