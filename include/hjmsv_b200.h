@@ -212,6 +212,17 @@ int32_t hjmsv_solver_price(hjmsv_solver* h, int32_t problem, double zr, double z
                            double* out);
 /* interpolate_at at natural_spot (f(0,0)/r0, 1, 0) (instruments.cpp:50-52,148) for all problems. */
 int32_t hjmsv_solver_spot_prices(hjmsv_solver* h, double* out);
+/* extract_greeks (instruments.cpp:90-132) of problem p's current level, on the
+ * device: rho = dU/dr~ and vega = dU/dv (computational-coordinate differences over
+ * j1, one-sided on the faces). scale_rate != 0 applies finish()'s rho /= r0
+ * (instruments.cpp:150-152). rho / vega are caller host buffers of nr*nv*ny
+ * doubles; either may be NULL. */
+int32_t hjmsv_solver_greeks(hjmsv_solver* h, int32_t problem, int32_t scale_rate, double* rho,
+                            double* vega);
+/* write_surface_csv's rows (job.cpp:300-310) at y-slice k, computed on the device:
+ * out[(i*nv + j)*5 + c] = (r0*z_r[i], z_v[j], U, rho/r0, vega)(i, j, k); only the
+ * slice crosses PCIe. */
+int32_t hjmsv_solver_surface(hjmsv_solver* h, int32_t problem, int32_t k, double* out);
 /* Device pointer of problem p's level (stable for the handle's lifetime). */
 int32_t hjmsv_solver_device_grid(hjmsv_solver* h, int32_t problem, double** dev_ptr);
 /* Elapsed device time of the last step_async batch (CUDA events on the handle's stream). */

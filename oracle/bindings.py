@@ -55,6 +55,7 @@ class Checker:
             "interpolate": (c_int, [P, PD, c_double, c_double, c_double, PD]),
             "spot_price": (c_int, [P, PD, PD]),
             "batch_run": (c_int, [P, c_int, C, c_int, PD, R]),
+            "extract_greeks": (c_int, [P, PD, c_int, PD, PD]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(self.lib, prefix + name)
@@ -136,6 +137,14 @@ class Checker:
         out = c_double()
         self._chk(self._f("interpolate")(ctypes.byref(cp), _ptr(g), zr, zv, zy, ctypes.byref(out)))
         return out.value
+
+    def greeks(self, p: ProblemSpec, grid, scale_rate: bool = True):
+        """extract_greeks (instruments.cpp:90-132) [+ finish()'s rho /= r0] -> (rho, vega)."""
+        cp = p.to_c()
+        g = np.ascontiguousarray(grid, dtype=np.float64).reshape(-1)
+        rho, vega = np.empty_like(g), np.empty_like(g)
+        self._chk(self._f("extract_greeks")(ctypes.byref(cp), _ptr(g), int(scale_rate), _ptr(rho), _ptr(vega)))
+        return rho.reshape(p.shape), vega.reshape(p.shape)
 
     def curve_eval(self, p: ProblemSpec, what: int, t) -> np.ndarray:
         c = p.to_c().curve

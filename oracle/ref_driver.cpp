@@ -416,6 +416,20 @@ int ref_spot_price(const hjmsv_problem* p, const double* grid_data, double* out)
     });
 }
 
+// extract_greeks (instruments.cpp:90-132) and finish()'s rho /= r0 (:150-152)
+int ref_extract_greeks(const hjmsv_problem* p, const double* grid_data, int scale_rate,
+                       double* rho_out, double* vega_out) {
+    return guarded([&] {
+        Grid3 g(to_axis(p->r), to_axis(p->v), to_axis(p->y));
+        std::memcpy(g.data.data(), grid_data, g.data.size() * sizeof(double));
+        auto [rho, vega] = extract_greeks(g);
+        if (scale_rate)
+            for (double& x : rho.data) x /= p->r0;
+        std::memcpy(rho_out, rho.data.data(), rho.data.size() * sizeof(double));
+        std::memcpy(vega_out, vega.data.data(), vega.data.size() * sizeof(double));
+    });
+}
+
 // caplet_ladder's worker pool (instruments.cpp:242-264) over independent
 // problems: each worker pulls the next index from an atomic counter and runs
 // the full march + spot readout. Used as the batched CPU baseline.

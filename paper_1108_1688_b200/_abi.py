@@ -95,6 +95,8 @@ SIGNATURES = {
     "hjmsv_solver_set_grid": (I32, [HP, I32, PD, I32]),
     "hjmsv_solver_price": (I32, [HP, I32, c_double, c_double, c_double, PD]),
     "hjmsv_solver_spot_prices": (I32, [HP, PD]),
+    "hjmsv_solver_greeks": (I32, [HP, I32, I32, PD, PD]),
+    "hjmsv_solver_surface": (I32, [HP, I32, I32, PD]),
     "hjmsv_solver_device_grid": (I32, [HP, I32, POINTER(PD)]),
     "hjmsv_solver_last_device_ms": (I32, [HP, PD]),
     "hjmsv_solver_last_launches": (I32, [HP, POINTER(c_int64)]),

@@ -160,6 +160,21 @@ class Solver:
         _check(self.lib.hjmsv_solver_spot_prices(self.h, _ptr(out)))
         return out
 
+    def greeks(self, problem: int = 0, scale_rate: bool = True):
+        """extract_greeks (instruments.cpp:90-132) of the current level, on the device;
+        scale_rate applies finish()'s rho /= r0 (instruments.cpp:150-152). -> (rho, vega)"""
+        rho, vega = np.empty(self.nr * self.nv * self.ny), np.empty(self.nr * self.nv * self.ny)
+        _check(self.lib.hjmsv_solver_greeks(self.h, problem, int(scale_rate), _ptr(rho), _ptr(vega)))
+        shape = (self.nr, self.nv, self.ny)
+        return rho.reshape(shape), vega.reshape(shape)
+
+    def surface(self, problem: int = 0, k: int = 0) -> np.ndarray:
+        """write_surface_csv's rows (job.cpp:300-310) at y-slice k: columns r_rate,
+        v_variance, price, rho_dprice_dr, vega_dprice_dv; shape (nr*nv, 5)."""
+        out = np.empty(self.nr * self.nv * 5)
+        _check(self.lib.hjmsv_solver_surface(self.h, problem, k, _ptr(out)))
+        return out.reshape(self.nr * self.nv, 5)
+
     def device_ptr(self, problem: int = 0) -> int:
         p = A.PD()
         _check(self.lib.hjmsv_solver_device_grid(self.h, problem, ctypes.byref(p)))

@@ -667,6 +667,47 @@ int32_t hjmsv_solver_get_grid(hjmsv_solver* h, int32_t problem, double* host_out
     });
 }
 
+int32_t hjmsv_solver_greeks(hjmsv_solver* h, int32_t problem, int32_t scale_rate, double* rho,
+                            double* vega) {
+    return guarded([&] {
+        if (!h) throw std::invalid_argument("null argument");
+        if (problem < 0 || problem >= h->P) throw std::invalid_argument("problem index out of range");
+        if (h->nr == 2 || h->nv == 2)
+            throw Failure(HJMSV_UNSUPPORTED, "extract_greeks needs 1 or >= 3 nodes per axis");
+        CK(cudaSetDevice(h->device));
+        // D / C are step workspaces, free between steps
+        greeks(h->view, problem, scale_rate ? 1 : 0, h->low[problem].r0, h->D, h->C, h->stream);
+        CK(cudaGetLastError());
+        if (rho)
+            CK(cudaMemcpyAsync(rho, h->D, sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->stream));
+        if (vega)
+            CK(cudaMemcpyAsync(vega, h->C, sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int32_t hjmsv_solver_surface(hjmsv_solver* h, int32_t problem, int32_t k, double* out) {
+    return guarded([&] {
+        if (!h || !out) throw std::invalid_argument("null argument");
+        if (problem < 0 || problem >= h->P) throw std::invalid_argument("problem index out of range");
+        if (k < 0 || k >= h->ny) throw std::invalid_argument("slice index out of range");
+        if (h->nr == 2 || h->nv == 2)
+            throw Failure(HJMSV_UNSUPPORTED, "extract_greeks needs 1 or >= 3 nodes per axis");
+        CK(cudaSetDevice(h->device));
+        const double r0 = h->low[problem].r0;
+        greeks(h->view, problem, 1, r0, h->D, h->C, h->stream);
+        const size_t rows = static_cast<size_t>(h->nr) * h->nv;
+        double* dev = dalloc<double>(rows * 5);
+        surface(h->view, problem, k, r0, h->D, h->C, dev, h->stream);
+        CK(cudaGetLastError());
+        const cudaError_t e = cudaMemcpyAsync(out, dev, sizeof(double) * rows * 5,
+                                              cudaMemcpyDeviceToHost, h->stream);
+        const cudaError_t e2 = e == cudaSuccess ? cudaStreamSynchronize(h->stream) : e;
+        dfree(dev);
+        CK(e2);
+    });
+}
+
 int32_t hjmsv_solver_set_grid(hjmsv_solver* h, int32_t problem, const double* host_in,
                               int32_t step_index) {
     return guarded([&] {

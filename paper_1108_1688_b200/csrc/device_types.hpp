@@ -130,6 +130,13 @@ void fast_prepare(const BatchView& v, cudaStream_t stream);  // builds v.fast fr
 int fast_stride(int nr, int nv, int ny);
 bool fast_supported(int nr, int nv, int ny);
 void reset_status(const BatchView& v, cudaStream_t stream);
+// extract_greeks of problem p's level (instruments.cpp:90-132); scale: rho /= r0
+// as finish() does (instruments.cpp:150-152). rho / vega may be null.
+void greeks(const BatchView& v, int p, int scale, double r0, double* rho, double* vega,
+            cudaStream_t stream);
+// write_surface_csv's rows at slice k (job.cpp:300-310): [nr*nv][5]
+void surface(const BatchView& v, int p, int k, double r0, const double* rho, const double* vega,
+             double* out, cudaStream_t stream);
 // U0[p] = terminal level of problem p for every p with tp[p].kind != TERM_HOST
 void device_terminal(const BatchView& v, const TermParam* tp, const int* host_kinds, double* U0,
                      cudaStream_t stream);

@@ -224,3 +224,25 @@ def test_device_terminal_matches_host(gpu, oracle, smoothing):
                 g = s.grid(q)
                 err = np.max(np.abs(g - ref)) / max(np.max(np.abs(ref)), 1e-300)
                 assert err <= 1e-14, f"terminal max rel err {err:.3e}"
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_device_greeks_and_surface(gpu, oracle, mode):
+    """extract_greeks + finish()'s rho scaling + write_surface_csv's slice on the device
+     vs the reference's loops on the same level: same operation order."""
+    p = W.make_problem(2, 3, nr=32, nv=16, ny=16, steps=20)
+    with hj.Solver([p], mode=mode) as s:
+        s.run()
+        g = s.grid(0)
+        rho, vega = s.greeks(0)
+        rho_u, _ = s.greeks(0, scale_rate=False)
+        surf = s.surface(0, k=0)
+    rho_ref, vega_ref = oracle.greeks(p, g)
+    rho_uref, _ = oracle.greeks(p, g, scale_rate=False)
+    for a, b in ((rho, rho_ref), (vega, vega_ref), (rho_u, rho_uref)):
+        assert np.max(np.abs(a - b)) <= 1e-15 * max(np.max(np.abs(b)), 1e-300)
+    rz = np.asarray(p.r.z)
+    vz = np.asarray(p.v.z)
+    ref = np.stack([np.repeat(p.r0 * rz, p.v.n), np.tile(vz, p.r.n), g[:, :, 0].ravel(),
+                    rho_ref[:, :, 0].ravel(), vega_ref[:, :, 0].ravel()], axis=1)
+    assert np.array_equal(surf, ref)

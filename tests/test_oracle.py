@@ -108,3 +108,16 @@ def test_divergence_reported_with_step(oracle):
     _, rep, code, msg = oracle.run(p, raise_on_error=False)
     if code:
         assert code in (3, 4) and msg.startswith(f"step {rep['failed_step']}/200: ")
+
+
+def test_greeks_restatement_bitexact_vs_reference(oracle, reference):
+    """extract_greeks (instruments.cpp:90-132) + finish()'s rho /= r0 on a solved
+    sinh-mesh caplet level: restatement == reference, bit for bit."""
+    p = W.make_problem(2, 2, nr=18, nv=9, ny=11, steps=15)
+    p.r = AxisSpec.sinh(p.strike / p.r0, 0.05, 0.0, 250.0, 18)
+    p.v = AxisSpec.sinh(0.5, 0.5, 0.0, 30.0, 9)
+    g, _, _, _ = reference.run(p)
+    for scale in (True, False):
+        r0_, v0_ = oracle.greeks(p, g, scale)
+        r1_, v1_ = reference.greeks(p, g, scale)
+        assert np.array_equal(r0_, r1_) and np.array_equal(v0_, v1_)
