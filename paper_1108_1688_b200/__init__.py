@@ -11,6 +11,7 @@ from .api import (Solver, run, price, apply_operator, douglas_step, thomas_batch
                   batch_run, device_count, HjmsvError, InvalidArgument, DomainError, LogicError,
                   SolverRuntimeError, SingularPivot, NonFinite, Diverged, Unsupported, CudaError)
 from . import workloads  # noqa: F401
+from . import drivers  # noqa: F401
 
 __all__ = ["AxisSpec", "ProblemSpec", "SolverConfig", "Solver", "run", "price", "apply_operator",
            "douglas_step", "thomas_batch", "batch_run", "device_count", "workloads"]

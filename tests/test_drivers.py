@@ -1,0 +1,55 @@
+"""Callers on the batch engine: caplet_ladder
+(instruments.cpp:238-266) and cmd_convergence's table (job.cpp:381-472)."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import paper_1108_1688_b200 as hj
+from paper_1108_1688_b200 import drivers
+from paper_1108_1688_b200 import workloads as W
+from paper_1108_1688_b200 import _abi as A
+
+
+def test_caplet_ladder_rejects_non_caplet():
+    with pytest.raises(ValueError):
+        drivers.caplet_ladder(W.make_problem(0, 0, nr=8, nv=4, ny=4, steps=2), [0.01])
+
+
+@pytest.mark.gpu
+def test_caplet_ladder_matches_per_strike_oracle(gpu, oracle):
+    base = W.make_problem(2, 4, nr=24, nv=12, ny=12, steps=30)
+    strikes = [0.01, 0.02, 0.035, 0.05]
+    out = drivers.caplet_ladder(base, strikes)
+    assert [k for k, _ in out] == strikes
+    prev = None
+    for k, price in out:
+        p = dataclasses.replace(base, strike=k)
+        g_ref, _, _, _ = oracle.run(p)
+        p_ref = oracle.spot_price(p, g_ref)
+        assert abs(price - p_ref) <= 1e-10 * abs(p_ref)
+        if prev is not None:  # caplet value falls with the strike
+            assert price <= prev + 1e-12
+        prev = price
+
+
+@pytest.mark.gpu
+def test_convergence_table_rows(gpu, oracle):
+    def make(nr, nv, ny):
+        return W.make_problem(0, 1, nr=nr, nv=nv, ny=ny, steps=1)
+
+    rows = drivers.convergence(make, nr_list=[16, 32], ny_list=[8, 16], nt_list=[20, 40],
+                               base=(16, 8, 8), config=hj.SolverConfig(steps_per_year=20))
+    sweeps = [r["sweep"] for r in rows]
+    assert sweeps == ["mesh", "mesh", "nt", "nt", "order"]
+    # each value is the device price of that mesh / step count; the error column is
+    # |price - p(0,T)| (price_zcb's closed-form reference)
+    for r in rows[:4]:
+        p = dataclasses.replace(make(r["nr"], r["nv"], r["ny"]), n_steps=0)
+        cfg = hj.SolverConfig(steps_per_year=r["steps_per_year"])
+        g_ref, _, _, _ = oracle.run(p, cfg)
+        p_ref = oracle.spot_price(p, g_ref)
+        assert abs(r["value"] - p_ref) <= 1e-10 * abs(p_ref)
+        disc = oracle.curve_eval(p, 0, np.array([p.maturity]))[0]
+        assert abs(r["error_or_delta"] - abs(r["value"] - disc)) <= 1e-12
+    assert np.isfinite(rows[-1]["error_or_delta"])
