@@ -1109,6 +1109,9 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async8s(unsigned dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
@@ -1125,8 +1128,8 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const int S = blockDim.y;
     const int nt = 16 * S;
     double* red = sm;                          // [16][S][8] reduced-system rows
-    double* ring = red + nt * 8;               // [kRing][4][nt] window prefetch
-    double* rt = ring + kRing * 4 * nt;        // [nr][8] r-table (FastR)
+    double* ring = red + nt * 8;               // [nt][kRing*4 + 1] window prefetch (padded)
+    double* rt = ring + (kRing * 4 + 1) * nt;  // [nr][8] r-table (FastR)
     double* fy = rt + v.nr * kFR;              // [2][nr] y-face values (YMAX, YMIN)
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
@@ -1176,7 +1179,11 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     double m0 = 0.0, m1 = 0.0, m2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, p0 = 0.0, p1 = 0.0, p2 = 0.0;
     double ce = 0.0, pe = 0.0;
     auto gptr = [&](int ii) { return col + static_cast<size_t>(min(max(ii, 0), nr - 1)) * SR; };
-    auto slot = [&](int q, int c) { return ring + (q * 4 + c) * nt + tid; };
+    // this thread's ring slots: 17-double stride between threads (conflict-free),
+    // compile-time offsets inside
+    double* const myring = ring + tid * (kRing * 4 + 1);
+    const unsigned myring_s = static_cast<unsigned>(__cvta_generic_to_shared(myring));
+    auto slot = [&](int q, int c) { return myring + q * 4 + c; };
     // the 16-lane group's edge lanes also carry their outside neighbour in k
     // (k-1 at tx 0, k+1 at tx 15; k+2 at k = 0 for the one-sided row)
     const bool edge = tx == 0 || (tx == 15 && !kN);
@@ -1193,10 +1200,10 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
 #pragma unroll
         for (int r = 0; r < kRing; ++r) {
             const double* g = gptr(a + 2 + r);
-            cp_async8(slot(r, 0), g - NY);
-            cp_async8(slot(r, 1), g);
-            cp_async8(slot(r, 2), g + NY);
-            if (edge) cp_async8(slot(r, 3), g + eoff);
+            cp_async8s(myring_s + 8 * (r * 4 + 0), g - NY);
+            cp_async8s(myring_s + 8 * (r * 4 + 1), g);
+            cp_async8s(myring_s + 8 * (r * 4 + 2), g + NY);
+            if (edge) cp_async8s(myring_s + 8 * (r * 4 + 3), g + eoff);
             cp_async_commit();
         }
     }
@@ -1228,6 +1235,14 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             d = fma(2.0, w2, 1.0);
             u = -(w2 + w1);
         }
+    };
+    // interior rows (0 < i < nr-1); a column that is not solved runs identity rows
+    const double ths = solve ? th : 0.0;
+    auto interior = [&](double g1s, double g4h, double& l, double& d, double& u) {
+        const double w2 = ths * g1s, w1 = ths * g4h;
+        l = w1 - w2;
+        d = fma(2.0, w2, 1.0);
+        u = -(w2 + w1);
     };
     auto rtab = [&](int i, double2& r01, double2& r23, double2& r45, double2& r67) {
         const double2* R2 = reinterpret_cast<const double2*>(rt + kFR * i);
@@ -1290,10 +1305,10 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             p0 = *slot(q, 0); p1 = *slot(q, 1); p2 = *slot(q, 2);
             if (edge) pe = *slot(q, 3);
             const double* g = gptr(a + r + kRing + 1);
-            cp_async8(slot(q, 0), g - NY);
-            cp_async8(slot(q, 1), g);
-            cp_async8(slot(q, 2), g + NY);
-            if (edge) cp_async8(slot(q, 3), g + eoff);
+            cp_async8s(myring_s + 8 * (q * 4 + 0), g - NY);
+            cp_async8s(myring_s + 8 * (q * 4 + 1), g);
+            cp_async8s(myring_s + 8 * (q * 4 + 2), g + NY);
+            if (edge) cp_async8s(myring_s + 8 * (q * 4 + 3), g + eoff);
             cp_async_commit();
         };
         // y-direction terms and the k faces (discretization.cpp:340-352)
@@ -1328,7 +1343,6 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             double2 r01, r23, r45, r67;
             rtab(i, r01, r23, r45, r67);
             const double g4h = g4(r01, r23, r45);
-            double s2;
             if (r == 0) {
                 if (a == 0) {
                     // face plane i = 0 (discretization.cpp:318-329): one-sided g4 term, no cross
@@ -1378,7 +1392,12 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                 // face plane i = nr-1: r_max is always Dirichlet and ranks first
                 x[r] = (r == M - 1 && i == nr - 1 && rmaxD) ? __ldg(fbp + k) - c1 : xv;
             }
-            coeffs(i, r01.x * vj, g4h, l, d, u, s2);
+            // rows a+1 .. a+14 are always interior; a+15 may be the r_max face
+            if (r == M - 1 && i == nr - 1 && rmaxD) {
+                l = 0.0; d = 1.0; u = 0.0;
+            } else {
+                interior(r01.x * vj, g4h, l, d, u);
+            }
         };
         ok = seg_solve<M>(M, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
         cp_async_wait<0>();
@@ -1414,7 +1433,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
 
 inline size_t pa_smem(int nr) {
     const int S = nr / 16, nt = 16 * S;
-    return sizeof(double) * (static_cast<size_t>(nt) * 8 + static_cast<size_t>(kRing) * 4 * nt +
+    return sizeof(double) * (static_cast<size_t>(nt) * 8 + static_cast<size_t>(kRing * 4 + 1) * nt +
                              static_cast<size_t>(nr) * (kFR + 2));
 }
 
