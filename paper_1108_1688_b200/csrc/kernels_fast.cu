@@ -284,6 +284,73 @@ __device__ __forceinline__ bool reduced_solve(double* E, int S, int stride, int&
     return ok;
 }
 
+// The same reduced system solved from both ends at once ("burn at both ends"):
+// lanes with back == false run the forward recurrence over pairs 0..mF-1, their
+// partner lanes (shfl_xor by `partner`) run the identical recurrence on the
+// reversed system over pairs S-2 .. mF. Reversal maps segment s to S-1-s and
+// swaps the roles of the end rows: first-row fields (yF, aF, bF) become
+// (yL, bL, aL) and vice versa, so both halves execute the same instructions.
+// The halves meet in a 2x2 solve at pair mF; each then back-substitutes its own
+// pairs into fields 6, 7 (p_t, q_t) in the original orientation.
+__device__ __forceinline__ bool reduced_solve_2way(double* E, int S, int stride, int fs, bool back,
+                                                   unsigned mask, int partner, int& bad_t) {
+    const int np = S - 1;
+    const int mF = (np + 1) >> 1, mB = np - mF;
+    const int fy0 = back ? 0 : 3, fa0 = back ? 2 : 4, fb0 = back ? 1 : 5;  // end row of s0
+    const int fy1 = back ? 3 : 0, fa1 = back ? 5 : 1, fb1 = back ? 4 : 2;  // first row of s1
+    const int sp = back ? 0 : 3, sq = back ? 2 : 4;                        // scratch Pp, Pq
+    double Pp = 0.0, Pq = 0.0;
+    bool ok = true;
+#pragma unroll 1
+    for (int k = 0; k < mF; ++k) {
+        if (k < (back ? mB : mF)) {
+            double* e0 = E + (back ? S - 1 - k : k) * stride;
+            const double* e1 = E + (back ? S - 2 - k : k + 1) * stride;
+            const double A = fma(e0[fa0 * fs], Pp, e0[fy0 * fs]);
+            const double B = fma(e0[fa0 * fs], Pq, e0[fb0 * fs]);
+            const double den = fma(-e1[fa1 * fs], B, 1.0);
+            if (fabs(den) < 1e-300 && ok) {
+                ok = false;
+                bad_t = back ? S - 2 - k : k + 1;
+            }
+            const double inv = frcp(den);
+            const double Qc = fma(e1[fa1 * fs], A, e1[fy1 * fs]) * inv;
+            const double Qd = e1[fb1 * fs] * inv;
+            Pp = fma(B, Qc, A);
+            Pq = B * Qd;
+            e0[6 * fs] = Qc;
+            e0[7 * fs] = Qd;
+            e0[sp * fs] = Pp;
+            e0[sq * fs] = Pq;
+        }
+    }
+    // meet: p_{mF-1} = PpF + PqF q_mF (forward), q_mF = PpB + PqB p_{mF-1} (backward)
+    const double oPp = __shfl_xor_sync(mask, Pp, partner);
+    const double oPq = __shfl_xor_sync(mask, Pq, partner);
+    const double PpF = back ? oPp : Pp, PqF = back ? oPq : Pq;
+    const double PpB = back ? Pp : oPp, PqB = back ? Pq : oPq;
+    const double pm = (PpF + PqF * PpB) / (1.0 - PqF * PqB);
+    const double qm = fma(PqB, pm, PpB);
+    double qn = back ? pm : qm;
+    const int n = back ? mB : mF;
+#pragma unroll 1
+    for (int k = n - 1; k >= 0; --k) {
+        double* e0 = E + (back ? S - 1 - k : k) * stride;
+        const double qs = fma(e0[7 * fs], qn, e0[6 * fs]);
+        const double ps = fma(e0[sq * fs], qn, e0[sp * fs]);
+        if (back) {  // reversed pair k is original pair t = S-2-k: p_t = qs, q_t = ps
+            double* et = E + (S - 2 - k) * stride;
+            et[6 * fs] = qs;
+            et[7 * fs] = ps;
+        } else {
+            e0[6 * fs] = ps;
+            e0[7 * fs] = qs;
+        }
+        qn = qs;
+    }
+    return ok;
+}
+
 // ============================================================ r-lines
 // Block = kLanesR consecutive k (same j) x S segments of M rows.
 template <int M>
@@ -1116,6 +1183,22 @@ __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
 }
+// one-shot bulk (TMA engine) copies of contiguous tables into shared memory,
+// completion tracked by an mbarrier (phase 0)
+__device__ __forceinline__ void bulk_init(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, unsigned bar) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(d), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_wait(unsigned bar) {
+    asm volatile("{\n .reg .pred P;\nWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n"
+                 " @!P bra WAIT_%=;\n}" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -1150,14 +1233,16 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const int a = sg * M;
     const size_t off = static_cast<size_t>(p) * v.N;
     const FT F = ftab(v, p);
-    // r-table and y-face values into shared memory asynchronously (group 0),
-    // overlapped with the window prologue below
-    for (int e = tid; e < nr * kFR / 2; e += nt) cp_async16(rt + 2 * e, F.R + 2 * e);
-    {
-        const double* fb0 = v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY;
-        for (int e = tid; e < 2 * nr; e += nt) cp_async8(fy + e, fb0 + e);
+    // r-table and y-face values into shared memory by two bulk copies, overlapped
+    // with the window prologue below
+    __shared__ alignas(8) unsigned long long tbar;
+    const unsigned tbar_s = static_cast<unsigned>(__cvta_generic_to_shared(&tbar));
+    if (tid == 0) {
+        const unsigned rbytes = nr * kFR * sizeof(double), ybytes = 2 * nr * sizeof(double);
+        bulk_init(tbar_s, rbytes + ybytes);
+        bulk_copy(rt, F.R, rbytes, tbar_s);
+        bulk_copy(fy, v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY, ybytes, tbar_s);
     }
-    cp_async_commit();
     const double c4 = __ldg(step_row(v, p, s) + ST_C4);
     const double2* V2 = reinterpret_cast<const double2*>(F.V + kFV * j);
     const double2 v01 = __ldg(V2), v23 = __ldg(V2 + 1);  // (V, G2), (G5, G3V)
@@ -1207,14 +1292,14 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             cp_async_commit();
         }
     }
+    __syncthreads();  // the mbarrier is initialised
+    bulk_wait(tbar_s);  // rt, fy have landed
     if (fail) {  // the problem failed in an earlier step (block-uniform)
         cp_async_wait<0>();
         return;
     }
     if (blockIdx.x == 0 && tid == 0) st.maxdelta_bits = 0ull;
     if (slowj) cp_async_wait<0>();
-    else cp_async_wait<kRing>();  // group 0 (tables) done; the ring may still be in flight
-    __syncthreads();  // rt, fy
 
     // row coefficients of I - th L_r at row i (g4h shared with the stencil)
     auto coeffs = [&](int i, double g1s, double g4h, double& l, double& d, double& u, double& s2) {
@@ -1321,9 +1406,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             if (k0)  // one-sided y row (discretization.cpp:346-352); ed = U(i, j, 2)
                 yd = order2y ? fma(4.0, kr, -ed) - 3.0 * u0 : 2.0 * (kr - u0);
             acc = fma(fma(a_i, vs6, t6), yd, acc);
-            double out = acc * dtm;
-            if (kface) out = fyk[i] - u0;
-            return out;
+            return acc * dtm;  // y-face Dirichlet columns are fixed up after the march
         };
         // dU0 at an interior row i from a window (mm, cc, pp)
         auto stencil = [&](int i, const double2& r01, const double2& r45, const double2& r67,
@@ -1408,13 +1491,28 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     double* E = red + sg * 8 * 16 + tx;
     E[0] = yF; E[16] = aF; E[32] = bF; E[48] = yL; E[64] = aL; E[80] = bL;
     __syncthreads();
-    if (sg == 0 && solve && S > 1) {
-        int bt = 0;
-        if (!reduced_solve(red + tx, S, 8 * 16, bt, 16)) record_pivot(st, s, 0, j * NY + k, bt * M);
+    if (sg < 2 && S > 1) {  // warp 0: segment rows 0 (forward) and 1 (backward) of every column
+        const unsigned mask = __ballot_sync(0xffffffffu, solve);
+        if (solve) {
+            int bt = 0;
+            if (!reduced_solve_2way(red + tx, S, 8 * 16, 16, sg == 1, mask, 16, bt))
+                record_pivot(st, s, 0, j * NY + k, bt * M);
+        }
     }
     __syncthreads();
     const double left = (solve && sg > 0) ? E[-8 * 16 + 6 * 16] : 0.0;  // p_{s-1} = x_{a-1}
     const double right = (solve && sg < S - 1) ? E[7 * 16] : 0.0;        // q_s = x_{a+m}
+    if (kface && !slowj) {
+        // y_max / y_min Dirichlet columns (identity rows): dU0 = face(t_next) - U
+        // (solver.cpp:111-116) wherever the r faces do not take precedence
+        // (discretization.cpp:153-192: r_max > y_max > v_max > r_min > y_min > v_min)
+#pragma unroll
+        for (int r = 0; r < M; ++r) {
+            const int i = a + r;
+            if (!((i == nr - 1 && rmaxD) || (i == 0 && rminD && !(kN && ymaxD))))
+                x[r] = fyk[i] - __ldg(col + static_cast<size_t>(i) * SR);
+        }
+    }
     double b = bL;
     double* __restrict__ dcol = v.D + off + static_cast<size_t>(j) * NY + k + static_cast<size_t>(a) * SR;
 #pragma unroll
