@@ -1812,7 +1812,16 @@ k_plane(BatchView v, int s) {
             }
         };
         __syncwarp();  // a line's LY segments lie in one warp
-        if (solve && sy == 0 && LY > 1) {
+        if constexpr (LY >= 8) {
+            // segment lanes 0 and 1 of each line solve its reduced system from both ends
+            const bool two = solve && sy < 2;
+            const unsigned m2 = __ballot_sync(0xffffffffu, two);
+            if (two) {
+                int bt = 0;
+                if (!reduced_solve_2way(ew, LY, TS, LPW, sy == 1, m2, 1, bt))
+                    record_pivot(st, s, 2, i * NV + j, bt * MS);
+            }
+        } else if (solve && sy == 0 && LY > 1) {  // short systems: one lane (measured faster)
             int bt = 0;
             if (!reduced_solve(ew, LY, TS, bt, LPW)) record_pivot(st, s, 2, i * NV + j, bt * MS);
         }
