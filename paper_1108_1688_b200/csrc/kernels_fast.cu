@@ -1011,7 +1011,8 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
     constexpr int kSegY = MY;
     constexpr int LY = NY / kSegY;
     constexpr int LPW = 32 / LY;
-    __shared__ double rs[8][32][8];
+    constexpr int TS = 8 * LPW + 1;                 // padded per-segment stride
+    __shared__ double rsp[8][LY * TS + 1];           // per warp: [segment][field][line]
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
     if (st.fail_step) return;
@@ -1102,17 +1103,25 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
     }
     double left = 0.0, right = 0.0;
     if (LY > 1) {
-        double* E = &rs[wid][base][0];
-        double* e = E + sy * 8;
-        e[0] = yF; e[1] = aF; e[2] = bF; e[3] = yL; e[4] = aL; e[5] = bL;
+        double* ew = &rsp[wid][lane / LY];
+        double* e = ew + sy * TS;
+        e[0] = yF; e[LPW] = aF; e[2 * LPW] = bF; e[3 * LPW] = yL; e[4 * LPW] = aL; e[5 * LPW] = bL;
         __syncwarp();
-        if (sy == 0 && solve) {
+        if constexpr (LY >= 8) {  // two-ended reduced solve by segment lanes 0 and 1
+            const bool two = solve && sy < 2;
+            const unsigned m2 = __ballot_sync(0xffffffffu, two);
+            if (two) {
+                int bt = 0;
+                if (!reduced_solve_2way(ew, LY, TS, LPW, sy == 1, m2, 1, bt))
+                    record_pivot(st, s, 2, line, bt * kSegY);
+            }
+        } else if (sy == 0 && solve) {
             int bt = 0;
-            if (!reduced_solve(E, LY, 8, bt)) record_pivot(st, s, 2, line, bt * kSegY);
+            if (!reduced_solve(ew, LY, TS, bt, LPW)) record_pivot(st, s, 2, line, bt * kSegY);
         }
         __syncwarp();
-        left = sy > 0 ? E[(sy - 1) * 8 + 6] : 0.0;
-        right = sy < LY - 1 ? e[7] : 0.0;
+        left = sy > 0 ? e[-TS + 6 * LPW] : 0.0;
+        right = sy < LY - 1 ? e[7 * LPW] : 0.0;
     }
     // x_r, then U += dU, Dirichlet values, max|dU|, guard (solver.cpp:163-176)
     double md = 0.0;
