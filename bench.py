@@ -244,10 +244,23 @@ def main():
     solver = hj.Solver(probs, device=local, mode=args.mode)
     flush = l2_flusher()
 
+    from paper_1108_1688_b200 import _abi as A
+    done_pts = [pts_per_march]
+    diverged = [0]
+
     def march():
         solver.reset()
         solver.step_async(solver.n_steps)
-        solver.synchronize()
+        code = solver.lib.hjmsv_solver_synchronize(solver.h)
+        if code not in (A.OK, A.DIVERGED, A.NONFINITE):
+            hj.api._check(code)
+        if code != A.OK:
+            # a problem whose scheme leaves the divergence bound stops where the
+            # reference's run() throws (guard_finite, solver.cpp:69-77; divergence
+            # parity); only the steps it actually took are counted
+            reps = [solver.report(q) for q in range(len(probs))]
+            done_pts[0] = sum(p.size * r["steps_done"] for p, r in zip(probs, reps))
+            diverged[0] = sum(1 for r in reps if r["status"] != A.OK)
         return solver.last_device_ms()
 
     if args.profile_only:
@@ -272,6 +285,7 @@ def main():
     if dist:
         dist.barrier()
     my_ms = sum(times)
+    pts_per_march = done_pts[0]
     t = torch.tensor([my_ms, float(pts_per_march)], dtype=torch.float64, device="cuda")
     if dist:
         tmax = t.clone()
@@ -323,7 +337,8 @@ def main():
             h = ctypes.c_void_p()
             code = lib.hjmsv_solver_create(arr, len(probs), ctypes.byref(cfg), local, mode, ctypes.byref(h))
             assert code == 0, lib.hjmsv_last_error()
-            assert lib.hjmsv_solver_run(h) == 0, lib.hjmsv_last_error()
+            rc = lib.hjmsv_solver_run(h)
+            assert rc in (A.OK, A.DIVERGED, A.NONFINITE), lib.hjmsv_last_error()
             assert lib.hjmsv_solver_spot_prices(h, _ptr(prices)) == 0
             off = 0
             for q, p in enumerate(probs):
@@ -363,6 +378,7 @@ def main():
                 "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"config {args.config}: {cs.description}",
                            "problems_per_rank": len(probs), "mode": args.mode,
+                           "diverged_problems": diverged[0],
                            "step": "one full march (all ADI steps) per bench step",
                            "l2": "256 MiB write between timed marches; a march's own state is "
                                  "carried step to step on device"},
