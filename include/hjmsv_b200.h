@@ -223,6 +223,24 @@ int32_t hjmsv_solver_greeks(hjmsv_solver* h, int32_t problem, int32_t scale_rate
  * out[(i*nv + j)*5 + c] = (r0*z_r[i], z_v[j], U, rho/r0, vega)(i, j, k); only the
  * slice crosses PCIe. */
 int32_t hjmsv_solver_surface(hjmsv_solver* h, int32_t problem, int32_t k, double* out);
+/* ---- Monte Carlo validator on the device (montecarlo.cpp:38-139) ----
+ * McConfig (montecarlo.hpp:15-24) without threads/observer. The device draws its
+ * normals from a counter-based generator (Philox4x32-10 + Box-Muller) keyed by
+ * (seed, path), so estimates are reproducible and independent of the launch
+ * shape, but they are a different sample from the reference's mt19937_64
+ * stream: parity with the reference is statistical (within standard errors). */
+typedef struct {
+    int64_t n_paths;
+    int32_t steps_per_year;
+    uint64_t seed;
+    int32_t full_truncation;
+} hjmsv_mc_config;
+void hjmsv_default_mc_config(hjmsv_mc_config* cfg);
+/* simulate_zcb / simulate_caplet (montecarlo.cpp:142-160) for problem p (its
+ * model, curve, instrument, maturity, payment, strike; the axes are unused).
+ * Writes McEstimate {mean, std_error, n_paths}. */
+int32_t hjmsv_mc_price(const hjmsv_problem* problem, const hjmsv_mc_config* cfg, int32_t device,
+                       double* mean, double* std_error, int64_t* n_paths);
 /* Device pointer of problem p's level (stable for the handle's lifetime). */
 int32_t hjmsv_solver_device_grid(hjmsv_solver* h, int32_t problem, double** dev_ptr);
 /* Elapsed device time of the last step_async batch (CUDA events on the handle's stream). */

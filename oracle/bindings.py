@@ -63,6 +63,9 @@ class Checker:
         if prefix == "ref_":
             self.lib.ref_mix_seed.restype = c_uint64
             self.lib.ref_mix_seed.argtypes = [c_uint64, c_uint64]
+            self.lib.ref_mc_price.restype = c_int
+            self.lib.ref_mc_price.argtypes = [P, POINTER(A.CMcConfig), c_int, PD, PD,
+                                              POINTER(ctypes.c_longlong)]
             self.lib.ref_g_factor.restype = c_int
             self.lib.ref_g_factor.argtypes = [c_double, c_double, PD]
 
@@ -145,6 +148,16 @@ class Checker:
         rho, vega = np.empty_like(g), np.empty_like(g)
         self._chk(self._f("extract_greeks")(ctypes.byref(cp), _ptr(g), int(scale_rate), _ptr(rho), _ptr(vega)))
         return rho.reshape(p.shape), vega.reshape(p.shape)
+
+    def mc_price(self, p: ProblemSpec, n_paths: int = 200000, steps_per_year: int = 96,
+                 seed: int = 20070423, full_truncation: bool = True, threads: int = 0):
+        """The reference's simulate_zcb / simulate_caplet (reference checker only)."""
+        cp = p.to_c()
+        cfg = A.CMcConfig(n_paths, steps_per_year, seed, int(full_truncation))
+        mean, se, n = c_double(), c_double(), ctypes.c_longlong()
+        self._chk(self.lib.ref_mc_price(ctypes.byref(cp), ctypes.byref(cfg), threads, ctypes.byref(mean),
+                                        ctypes.byref(se), ctypes.byref(n)))
+        return mean.value, se.value, n.value
 
     def curve_eval(self, p: ProblemSpec, what: int, t) -> np.ndarray:
         c = p.to_c().curve

@@ -430,6 +430,29 @@ int ref_extract_greeks(const hjmsv_problem* p, const double* grid_data, int scal
     });
 }
 
+// simulate_zcb / simulate_caplet (montecarlo.cpp:142-160): the reference's own
+// Monte Carlo (mt19937_64 per 8192-path batch), the statistical check of the
+// device validator
+int ref_mc_price(const hjmsv_problem* p, const hjmsv_mc_config* c, int threads, double* mean,
+                 double* std_error, long long* n_paths) {
+    return guarded([&] {
+        McConfig mc;
+        mc.n_paths = c->n_paths;
+        mc.steps_per_year = c->steps_per_year;
+        mc.seed = c->seed;
+        mc.full_truncation = c->full_truncation != 0;
+        mc.threads = threads;
+        const InitialCurve curve = to_curve(p->curve);
+        const ModelParams mp = to_model(p->model);
+        const McEstimate est = p->instrument == HJMSV_INSTRUMENT_CAPLET
+                                   ? simulate_caplet(to_caplet(*p), curve, mp, mc)
+                                   : simulate_zcb(p->maturity, curve, mp, mc);
+        *mean = est.mean;
+        *std_error = est.std_error;
+        *n_paths = est.n_paths;
+    });
+}
+
 // caplet_ladder's worker pool (instruments.cpp:242-264) over independent
 // problems: each worker pulls the next index from an atomic counter and runs
 // the full march + spot readout. Used as the batched CPU baseline.

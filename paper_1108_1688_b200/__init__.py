@@ -7,7 +7,7 @@ importing the solver API without it raises ImportError — there is no CPU path.
 """
 from . import _abi  # noqa: F401
 from .problem import AxisSpec, ProblemSpec, SolverConfig, mix_seed  # noqa: F401
-from .api import (Solver, run, price, apply_operator, douglas_step, thomas_batch,  # noqa: F401
+from .api import (Solver, run, price, mc_price, apply_operator, douglas_step, thomas_batch,  # noqa: F401
                   batch_run, device_count, HjmsvError, InvalidArgument, DomainError, LogicError,
                   SolverRuntimeError, SingularPivot, NonFinite, Diverged, Unsupported, CudaError)
 from . import workloads  # noqa: F401

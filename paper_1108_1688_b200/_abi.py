@@ -62,6 +62,11 @@ class CSolverConfig(ctypes.Structure):
                 ("smoothing_subsamples", c_int32), ("divergence_bound", c_double)]
 
 
+class CMcConfig(ctypes.Structure):
+    _fields_ = [("n_paths", ctypes.c_int64), ("steps_per_year", c_int32), ("seed", ctypes.c_uint64),
+                ("full_truncation", c_int32)]
+
+
 class CReport(ctypes.Structure):
     _fields_ = [("wall_seconds", c_double), ("n_steps", c_int32), ("steps_done", c_int32),
                 ("last_max_delta", c_double), ("nan_guard_ok", c_int32), ("status", c_int32),
@@ -75,6 +80,9 @@ class CReport(ctypes.Structure):
 I32, HP = c_int32, c_void_p
 SIGNATURES = {
     "hjmsv_default_solver_config": (None, [POINTER(CSolverConfig)]),
+    "hjmsv_default_mc_config": (None, [POINTER(CMcConfig)]),
+    "hjmsv_mc_price": (I32, [POINTER(CProblem), POINTER(CMcConfig), I32, PD, PD,
+                             POINTER(ctypes.c_int64)]),
     "hjmsv_last_error": (ctypes.c_char_p, []),
     "hjmsv_abi_version": (I32, []),
     "hjmsv_device_count": (I32, []),

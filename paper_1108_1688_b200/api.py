@@ -277,5 +277,20 @@ def batch_run(problems: Sequence[ProblemSpec], config: Optional[SolverConfig] = 
     return prices, reps, g
 
 
+def mc_price(problem: ProblemSpec, n_paths: int = 200000, steps_per_year: int = 96,
+             seed: int = 20070423, full_truncation: bool = True, device: int = 0):
+    """Monte Carlo validator on the device (simulate_zcb / simulate_caplet,
+    montecarlo.cpp:142-160) -> (mean, std_error, n_paths). Counter-based normals:
+    a different sample from the reference's mt19937_64 stream (compare within
+    standard errors)."""
+    lib = A.load()
+    cp = problem.to_c()
+    cfg = A.CMcConfig(n_paths, steps_per_year, seed, int(full_truncation))
+    mean, se, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+    _check(lib.hjmsv_mc_price(ctypes.byref(cp), ctypes.byref(cfg), device, ctypes.byref(mean),
+                              ctypes.byref(se), ctypes.byref(n)))
+    return mean.value, se.value, n.value
+
+
 def device_count() -> int:
     return int(A.load().hjmsv_device_count())

@@ -708,6 +708,82 @@ int32_t hjmsv_solver_surface(hjmsv_solver* h, int32_t problem, int32_t k, double
     });
 }
 
+void hjmsv_default_mc_config(hjmsv_mc_config* cfg) {
+    if (!cfg) return;
+    cfg->n_paths = 200000;  // McConfig defaults, montecarlo.hpp:15-24
+    cfg->steps_per_year = 96;
+    cfg->seed = 20070423ull;
+    cfg->full_truncation = 1;
+}
+
+int32_t hjmsv_mc_price(const hjmsv_problem* problem, const hjmsv_mc_config* cfg, int32_t device,
+                       double* mean, double* std_error, int64_t* n_paths) {
+    return guarded([&] {
+        if (!problem || !cfg || !mean || !std_error || !n_paths) throw std::invalid_argument("null argument");
+        const McSetup m = lower_mc(*problem, *cfg);
+        *n_paths = cfg->n_paths;
+        if (m.horizon == 0.0) {  // simulate(): horizon 0 returns payout(0, 0, 1), montecarlo.cpp:92
+            *mean = 1.0;
+            *std_error = 0.0;
+            return;
+        }
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) throw std::invalid_argument("no such CUDA device");
+        CK(cudaSetDevice(device));
+        McParams mp{};
+        mp.n_paths = cfg->n_paths;
+        mp.n_steps = m.n_steps;
+        mp.full_truncation = cfg->full_truncation ? 1 : 0;
+        mp.seed = cfg->seed;
+        mp.dt = m.dt;
+        mp.sqrt_dt = m.sqrt_dt;
+        mp.decay_y = m.decay_y;
+        mp.decay_h = m.decay_h;
+        mp.f0 = m.f0;
+        const hjmsv_model& md = problem->model;
+        mp.kappa = md.kappa;
+        mp.theta = md.theta;
+        mp.rho = md.rho;
+        mp.sq1mr2 = std::sqrt(1.0 - md.rho * md.rho);
+        mp.lambda = md.lambda;
+        mp.gamma = md.gamma;
+        mp.eps = md.eps;
+        mp.caplet = m.caplet;
+        mp.accrual = m.accrual;
+        mp.ratio = m.ratio;
+        mp.g = m.g;
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        const long long want = (cfg->n_paths + 255) / 256;
+        const int blocks = static_cast<int>(std::min<long long>(want, 8LL * sms));
+        double* f = dalloc<double>(m.f_next.size());
+        double* part = dalloc<double>(2 * static_cast<size_t>(blocks));
+        std::vector<double> ph(2 * static_cast<size_t>(blocks));
+        cudaError_t e = cudaMemcpy(f, m.f_next.data(), sizeof(double) * m.f_next.size(),
+                                   cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) {
+            mc_simulate(mp, f, part, blocks, nullptr);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess)
+            e = cudaMemcpy(ph.data(), part, sizeof(double) * ph.size(), cudaMemcpyDeviceToHost);
+        dfree(f);
+        dfree(part);
+        CK(e);
+        double sum = 0.0, sum_sq = 0.0;  // block order: independent of scheduling
+        for (int b = 0; b < blocks; ++b) {
+            sum += ph[2 * b];
+            sum_sq += ph[2 * b + 1];
+        }
+        const double n = static_cast<double>(cfg->n_paths);
+        const double mu = sum / n;  // simulate(), montecarlo.cpp:130-137
+        const double var = cfg->n_paths > 1 ? std::max(0.0, (sum_sq - n * mu * mu) / (n - 1)) : 0.0;
+        *mean = mu;
+        *std_error = std::sqrt(var / n);
+    });
+}
+
 int32_t hjmsv_solver_set_grid(hjmsv_solver* h, int32_t problem, const double* host_in,
                               int32_t step_index) {
     return guarded([&] {

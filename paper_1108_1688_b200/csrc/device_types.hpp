@@ -130,6 +130,20 @@ void fast_prepare(const BatchView& v, cudaStream_t stream);  // builds v.fast fr
 int fast_stride(int nr, int nv, int ny);
 bool fast_supported(int nr, int nv, int ny);
 void reset_status(const BatchView& v, cudaStream_t stream);
+// Monte Carlo validator (kernels_mc.cu): run_path's constants (montecarlo.cpp:38-79)
+struct McParams {
+    long long n_paths;
+    int n_steps;
+    int full_truncation;
+    unsigned long long seed;
+    double dt, sqrt_dt, decay_y, decay_h, f0;
+    double kappa, theta, rho, sq1mr2, lambda, gamma, eps;
+    int caplet;
+    double accrual, ratio, g;
+};
+// partial[2*b] = sum, partial[2*b+1] = sum of squares of block b's path samples
+void mc_simulate(const McParams& mp, const double* f_next, double* partial, int blocks,
+                 cudaStream_t stream);
 // extract_greeks of problem p's level (instruments.cpp:90-132); scale: rho /= r0
 // as finish() does (instruments.cpp:150-152). rho / vega may be null.
 void greeks(const BatchView& v, int p, int scale, double r0, double* rho, double* vega,

@@ -455,4 +455,36 @@ std::vector<double> build_fast_tables(const Lowered& L, const hjmsv_solver_confi
     return t;
 }
 
+McSetup lower_mc(const hjmsv_problem& p, const hjmsv_mc_config& c) {
+    validate_model(p.model);  // simulate(): params.validate(), montecarlo.cpp:86-91
+    if (c.n_paths < 1) throw std::invalid_argument("n_paths must be >= 1");
+    if (c.steps_per_year < 1) throw std::invalid_argument("mc steps_per_year must be >= 1");
+    McSetup m;
+    const Curve curve = import_curve(p.curve);
+    if (p.instrument == HJMSV_INSTRUMENT_CAPLET) {  // CapletSpec::validate, model.cpp:35-39
+        if (p.maturity <= 0.0) throw std::invalid_argument("caplet expiry must be positive");
+        if (p.payment <= p.maturity)
+            throw std::invalid_argument("caplet payment date must exceed expiry");
+        if (p.strike <= 0.0) throw std::invalid_argument("caplet strike must be positive");
+        m.caplet = 1;
+        m.accrual = 1.0 + (p.payment - p.maturity) * p.strike;  // model.hpp:55
+        m.ratio = curve.discount(p.payment) / curve.discount(p.maturity);
+        m.g = g_factor(p.payment - p.maturity, p.model.kappa);
+    } else if (p.instrument != HJMSV_INSTRUMENT_ZCB) {
+        throw std::invalid_argument("Monte Carlo prices ZCB and caplet instruments");
+    }
+    if (p.maturity < 0.0) throw std::invalid_argument("horizon must be nonnegative");
+    m.horizon = p.maturity;
+    m.f0 = curve.forward(0.0);
+    if (p.maturity == 0.0) return m;
+    m.n_steps = std::max(1, static_cast<int>(std::lround(c.steps_per_year * p.maturity)));
+    m.dt = p.maturity / m.n_steps;  // run_path, montecarlo.cpp:44-48
+    m.sqrt_dt = std::sqrt(m.dt);
+    m.decay_y = std::exp(-2.0 * p.model.kappa * m.dt);
+    m.decay_h = std::exp(-p.model.kappa * m.dt);
+    m.f_next.resize(m.n_steps);
+    for (int s = 0; s < m.n_steps; ++s) m.f_next[s] = curve.forward(s * m.dt + m.dt);
+    return m;
+}
+
 }  // namespace hjmsv_b200

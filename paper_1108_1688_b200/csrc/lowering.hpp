@@ -51,6 +51,17 @@ void locate_point(const Lowered& L, double zr, double zv, double zy, long long i
 
 hjmsv_solver_config default_config();
 
+/// Host side of the Monte Carlo validator (montecarlo.cpp:83-139): validated
+/// model, per-step forward curve f(0, t_s + dt) and the payout scalars.
+struct McSetup {
+    int n_steps = 0;
+    double dt = 0.0, sqrt_dt = 0.0, decay_y = 0.0, decay_h = 0.0, f0 = 0.0;
+    std::vector<double> f_next;   // f(0, (s+1) dt), s = 0..n_steps-1
+    int caplet = 0;
+    double accrual = 0.0, ratio = 0.0, g = 0.0, horizon = 0.0;
+};
+McSetup lower_mc(const hjmsv_problem& p, const hjmsv_mc_config& c);
+
 /// FAST-mode factor tables (layout: FastR/FastV/FastY in device_types.hpp).
 std::vector<double> build_fast_tables(const Lowered& L, const hjmsv_solver_config& cfg,
                                       double theta_dt);
