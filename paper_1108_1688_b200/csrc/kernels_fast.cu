@@ -1569,7 +1569,7 @@ struct PlaneGeom {
     static constexpr int NT = NTX;
     static constexpr int YROUNDS = (RV * LY + NT - 1) / NT;
     static constexpr int TILE = RV * PITCH;
-    static constexpr int VT = 5 * NV;             // v tables: RP B E BF BB
+    static constexpr int VT = 6 * NV + 2;         // v tables: RP B E BF BB V, + the plane's 2 y-face values
     static constexpr int YT = 2 * (LY * 17);      // y tables: (S6, T6) pairs, 17-pair segments
     static constexpr int CAR = 2 * SV * NY;       // v carries (all segments, both directions)
     static constexpr int EY = (NT / 32) * ((NY / 16) * (8 * (32 / (NY / 16)) + 1) + 1);  // per warp: LY x TS + 1
@@ -1590,7 +1590,7 @@ k_plane(BatchView v, int s) {
     constexpr int MS = G::MS, LY = G::LY, SV = G::SV, SVL = G::SVL, RV = G::RV, NT = G::NT;
     extern __shared__ double sm[];
     double* tile = sm;
-    double* vtab = tile + G::TILE;   // [5][NV]: RP, B, E, BF, BB
+    double* vtab = tile + G::TILE;   // [6][NV]: RP, B, E, BF, BB, V; then y-face values (YMAX, YMIN)
     double* ytab = vtab + G::VT;     // [LY*17] (S6, T6) pairs
     double* car = ytab + G::YT;      // [2][SV][NY]
     double* ey = car + G::CAR;       // [NT/LY lines][LY][8]
@@ -1618,6 +1618,10 @@ k_plane(BatchView v, int s) {
     const size_t off = static_cast<size_t>(p) * v.N;
     const size_t pb = off + (static_cast<size_t>(i) * NV + j0) * NY;  // first row of this CTA
     const FT F = ftab(v, p);
+    // per-plane scalars, loaded while the plane is staged
+    const ProblemConst& pc = v.pc[p];
+    const double th = pc.theta_dt, bound = pc.bound;
+    const double a_i = __ldg(F.R + kFR * i + FR_A), react = __ldg(F.R + kFR * i + FR_REACT);
     {  // staged even for a failed problem: the loads need not wait for the status word
         if (tid == 0) {  // U rows -> L2 early, so the update's loads hit L2
             constexpr unsigned bytes = RV * NY * sizeof(double);
@@ -1643,7 +1647,10 @@ k_plane(BatchView v, int s) {
             vtab[2 * NV + e] = Vr[FV_E];
             vtab[3 * NV + e] = Vr[FV_BF];
             vtab[4 * NV + e] = Vr[FV_BB];
+            vtab[5 * NV + e] = Vr[FV_V];
         }
+        if (tid < 2)  // this plane's y-face values at t_next: YMAX, YMIN
+            vtab[6 * NV + tid] = __ldg(v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY + tid * nr + i);
         for (int e = tid; e < NY; e += NT) {  // padded so the segments hit distinct banks
             const int cc = 2 * ((e >> 4) * 17 + (e & 15));
             ytab[cc] = F.Y[kFY * e + FY_S6];
@@ -1733,12 +1740,7 @@ k_plane(BatchView v, int s) {
     if (!live_p) return;  // no cluster barrier follows
 
     // ---- y-lines (rows j) + update, in rounds of NT segment tasks
-    const ProblemConst& pc = v.pc[p];
-    const double th = pc.theta_dt;
-    const double a_i = F.R[kFR * i + FR_A], react = F.R[kFR * i + FR_REACT];
     const double dint = fma(th, react, 1.0);
-    const double bound = pc.bound;
-    const double* fby = v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY;  // y faces [nr] x2
     const bool wmd = v.want_md;
     double md = 0.0;
 #pragma unroll 1
@@ -1754,7 +1756,7 @@ k_plane(BatchView v, int s) {
         for (int r = 0; r < MS; ++r) x[r] = live ? tile[G::at(jl, a + r)] : 0.0;
         double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
         if (solve) {
-            const double h1 = a_i * F.V[kFV * j + FV_V];
+            const double h1 = a_i * vtab[5 * NV + j];
             double lr[MS];
             double g60 = 0.0;
 #pragma unroll
@@ -1858,8 +1860,8 @@ k_plane(BatchView v, int s) {
 #pragma unroll
                 for (int r = 0; r < MS; ++r) un[r] = fval(v, p, dface(v, i, j, a + r), i, a + r);
             } else {
-                if (sy == 0 && yminD) un[0] = __ldg(fby + nr + i);
-                if (sy == LY - 1 && ymaxD) un[MS - 1] = __ldg(fby + i);
+                if (sy == 0 && yminD) un[0] = vtab[6 * NV + 1];
+                if (sy == LY - 1 && ymaxD) un[MS - 1] = vtab[6 * NV];
             }
 #pragma unroll
             for (int r = 0; r < MS; ++r)  // guard_finite (solver.cpp:69-77)
