@@ -1266,6 +1266,9 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const double* fbp = v.fb + static_cast<size_t>(p) * v.fb_stride;
     const double* fyk = fy + (kN ? 0 : nr);
     const bool kface = (kN && ymaxD) || (k0 && yminD);
+    // r-face values this thread needs (first / last segment), loaded up front
+    const double rminv = (sg == 0 && rminD) ? __ldg(fbp + NY + k) : 0.0;
+    const double rmaxv = (a + M == nr && rmaxD) ? __ldg(fbp + k) : 0.0;
     const double* __restrict__ col = v.U + off + static_cast<size_t>(j) * NY + k;
     double x[M], cs[M], al[M];
     // window for columns j-1 (0), j (1), j+1 (2): m = row ic-1, c = ic, p = ic+1;
@@ -1447,7 +1450,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                     acc = fma(v23.x, c2 - c0, acc);
                     double x0 = yterm(0, u0, acc, r67.y, ce);
                     // r_min Dirichlet ranks below r_max / y_max / v_max (discretization.cpp:153-192)
-                    if (rminD && !(kN && ymaxD)) x0 = __ldg(fbp + NY + k) - u0;
+                    if (rminD && !(kN && ymaxD)) x0 = rminv - u0;
                     x[0] = x0;
                     // the super2 fold needs row 1's rhs (solver.cpp:28-40)
                     double2 q01, q23, q45, q67;
@@ -1482,7 +1485,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                 shift(r);
                 const double xv = stencil(i, r01, r45, r67, g4h, m0, m1, m2, c0, c1, c2, p0, p1, p2, ce);
                 // face plane i = nr-1: r_max is always Dirichlet and ranks first
-                x[r] = (r == M - 1 && i == nr - 1 && rmaxD) ? __ldg(fbp + k) - c1 : xv;
+                x[r] = (r == M - 1 && i == nr - 1 && rmaxD) ? rmaxv - c1 : xv;
             }
             // rows a+1 .. a+14 are always interior; a+15 may be the r_max face
             if (r == M - 1 && i == nr - 1 && rmaxD) {
