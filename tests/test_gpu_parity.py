@@ -10,6 +10,7 @@ import pytest
 import paper_1108_1688_b200 as hj
 from paper_1108_1688_b200 import workloads as W
 from paper_1108_1688_b200.problem import AxisSpec
+from paper_1108_1688_b200 import _abi as A
 from oracle import bindings as B
 
 pytestmark = pytest.mark.gpu
@@ -246,3 +247,56 @@ def test_device_greeks_and_surface(gpu, oracle, mode):
     ref = np.stack([np.repeat(p.r0 * rz, p.v.n), np.tile(vz, p.r.n), g[:, :, 0].ravel(),
                     rho_ref[:, :, 0].ravel(), vega_ref[:, :, 0].ravel()], axis=1)
     assert np.array_equal(surf, ref)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_config2_full_shape_prefix(gpu, oracle, mode):
+    """The config-2 grid (128x64x64) through the two-pass FAST kernels (pass A
+    k_pa<64,64>, pass B k_plane<64,64>), 30 of its 500 steps."""
+    p = W.make_problem(2, 5)
+    grids, _, _, _ = solve([p], mode, steps=30)
+    assert_parity(p, grids[0], None, oracle, mode, steps=30)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_sinh_mesh_two_pass_shape(gpu, oracle, mode):
+    """Non-uniform Jacobians on a shape served by the two-pass kernels (64x32x32)."""
+    p = W.make_problem(2, 6, nr=64, nv=32, ny=32, steps=50)
+    p.r = AxisSpec.sinh(p.strike / p.r0, 0.05, 0.0, 250.0, 64)
+    p.v = AxisSpec.sinh(0.5, 0.5, 0.0, 30.0, 32)
+    p.y = AxisSpec.sinh(0.0, 0.05, 0.0, 250.0, 32)
+    grids, prices, _, _ = solve([p], mode)
+    assert_parity(p, grids[0], prices[0], oracle, mode)
+
+
+FACE_CASES = {
+    "all_dirichlet": ((0, 0, 0, 0, 0, 0), 2, 2),
+    "rmin_dirichlet": ((0, 0, 1, 0, 2, 0), 2, 2),
+    "vmin_dirichlet": ((1, 0, 0, 0, 2, 0), 2, 2),
+    "ymin_dirichlet": ((1, 0, 1, 0, 0, 0), 2, 2),
+    "first_order_rows": ((1, 0, 1, 0, 2, 0), 1, 1),
+}
+
+
+@pytest.mark.parametrize("case", sorted(FACE_CASES))
+@pytest.mark.parametrize("mode", MODES)
+def test_custom_face_rules_two_pass(gpu, oracle, mode, case):
+    """BoundarySpec face rules beyond the instruments' (discretization.cpp:153-192,
+    precedence r_max > y_max > v_max > r_min > y_min > v_min) and first-order
+    boundary rows, on the two-pass shape 32^3."""
+    rules, y_order, r_order = FACE_CASES[case]
+    p = W.make_problem(0, 3, nr=32, nv=32, ny=32, steps=40)
+    p.instrument = A.INSTRUMENT_CUSTOM
+    p.face_rule = rules
+    # every face: P(t, T) (ZCB closed form); the v_max face: P(t,T) - 0.5 P(t, 1.5 T)
+    zcb = (1, 1.0, p.maturity, 0.0, 0.0)
+    p.face_value = (zcb, zcb, zcb, (2, 1.0, p.maturity, 0.5, 1.5 * p.maturity), zcb, zcb)
+    rng = np.random.default_rng(7)
+    p.initial_grid = 1.0 + 0.01 * rng.standard_normal(p.shape)
+    cfg = hj.SolverConfig(y_boundary_order=y_order, r_boundary_order=r_order)
+    with hj.Solver([p], mode=mode, config=cfg) as s:
+        s.run()
+        g = s.grid(0)
+    g_ref, _, _, _ = oracle.run(p, cfg)
+    err = B.normwise_rel(g, g_ref)
+    assert err <= tol_for(mode), f"{case}: grid normwise rel err {err:.3e}"
