@@ -1667,7 +1667,32 @@ k_plane(BatchView v, int s) {
     const bool vwork = live_p && !planeD;
 
     // ---- v-lines (columns k), skip columns on y Dirichlet faces (solver.cpp:142)
-    if (!planeD) {  // uniform over the cluster
+    if (CS == 1 && NV <= 32 && !planeD) {
+        // short columns: one thread per column runs the table LU's two
+        // substitutions as plain recurrences (no segment carries or extra
+        // passes; measured faster for 32-row columns, slower for longer ones)
+        if (vwork && tid < NY) {
+            const int k = tid;
+            if (!((k == 0 && yminD) || (k == NY - 1 && ymaxD))) {
+                double loc = 0.0;
+                int bad = -1;
+#pragma unroll 8
+                for (int j = 0; j < NV; ++j) {
+                    if (isnan(vtab[j]) && bad < 0) bad = j;  // singular v pivot (table NaN)
+                    loc = fma(vtab[NV + j], loc, vtab[j] * tile[G::at(j, k)]);
+                    tile[G::at(j, k)] = loc;
+                }
+                if (bad >= 0) record_pivot(st, s, 1, i * NY + k, bad);
+                double xb = 0.0;
+#pragma unroll 8
+                for (int j = NV - 1; j >= 0; --j) {
+                    xb = fma(vtab[2 * NV + j], xb, tile[G::at(j, k)]);
+                    tile[G::at(j, k)] = xb;
+                }
+            }
+        }
+        __syncthreads();
+    } else if (!planeD) {  // uniform over the cluster
         if (vwork) {
             for (int task = tid; task < NY * SVL; task += NT) {
                 const int k = task % NY, sl = task / NY, a = sl * MS;
