@@ -1261,7 +1261,13 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const double vs6 = vj * y01.x, t6 = y01.y;
     const double th = pc.theta_dt, dtm = pc.dt;
     const bool rmaxD = dir(v, F_RMAX), rminD = dir(v, F_RMIN);
-    const bool slowj = j == 0 || j == NV - 1;  // block-uniform
+    // v-face rows (block-uniform): j = nv-1 is the v_max Dirichlet face (an early,
+    // load-store-only path); j = 0 is Dirichlet (same path) or the degenerate
+    // one-sided row, which takes the generic out-of-line stencil
+    const bool vminD = dir(v, F_VMIN), vmaxD = dir(v, F_VMAX);
+    const bool jlo = j == 0, jhi = j == NV - 1;
+    const bool jdir = (jhi && vmaxD) || (jlo && vminD);
+    const bool slowj = (jlo || jhi) && !jdir;
     const bool order2y = v.y_order != 1, order2r = v.r_order != 1;
     const double* fbp = v.fb + static_cast<size_t>(p) * v.fb_stride;
     const double* fyk = fy + (kN ? 0 : nr);
@@ -1285,7 +1291,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     // (k-1 at tx 0, k+1 at tx 15; k+2 at k = 0 for the one-sided row)
     const bool edge = tx == 0 || (tx == 15 && !kN);
     const int eoff = tx == 0 ? (k0 ? 2 : -1) : 1;
-    if (!slowj) {
+    if (!slowj && !jdir) {
         const double* q = gptr(a - 1);
         m0 = __ldg(q - NY); m1 = __ldg(q); m2 = __ldg(q + NY);
         q = gptr(a);
@@ -1311,6 +1317,38 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         return;
     }
     if (blockIdx.x == 0 && tid == 0) st.maxdelta_bits = 0ull;
+    // the face buffer of step s+1 (read from the next step on), spread over the
+    // grid's threads after the march (replaces a k_faces launch per step)
+    auto next_faces = [&] {
+        if (v.fb_next && s + 1 < v.S) {
+            const int nb = gridDim.x;
+            double* fbn = v.fb_next + static_cast<size_t>(p) * v.fb_stride;
+            for (int e = tid * nb + blockIdx.x; e < v.fb_stride; e += nt * nb)
+                fbn[e] = face_entry(v, p, s + 1, e);
+        }
+    };
+    if (jdir) {
+        // a Dirichlet v face: every column is an identity line, dU1 = dU0 =
+        // face(t_next) - U (solver.cpp:111-116, 127), with the face precedence
+        // r_max > y_max > v_max > r_min > y_min > v_min (discretization.cpp:153-192)
+        const double* fv = fbp + 2 * NY + 2 * nr + (jhi ? 0 : nr * NY) + k;
+        double* dcol = v.D + off + static_cast<size_t>(j) * NY + k;
+#pragma unroll 4
+        for (int r = 0; r < M; ++r) {
+            const int i = a + r;
+            const double u0 = __ldg(col + static_cast<size_t>(i) * SR);
+            double f = __ldg(fv + static_cast<size_t>(i) * NY);
+            if (!jhi) {  // v_min ranks last
+                if (i == 0 && rminD) f = rminv;
+                if (k0 && yminD) f = fyk[i];
+            }
+            if (kN && ymaxD) f = fyk[i];
+            if (i == nr - 1 && rmaxD) f = rmaxv;
+            dcol[static_cast<size_t>(i) * SR] = f - u0;
+        }
+        next_faces();
+        return;
+    }
     if (slowj) cp_async_wait<0>();
 
     // row coefficients of I - th L_r at row i (g4h shared with the stencil)
@@ -1532,13 +1570,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         if (r < M - 1) b = -cs[r] * b;
         dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(al[r], left, x[r]));
     }
-    // the face buffer of step s+1 (read from the next step on), spread over the
-    // grid's threads after the march (replaces a k_faces launch per step)
-    if (v.fb_next && s + 1 < v.S) {
-        const int nb = gridDim.x;
-        double* fbn = v.fb_next + static_cast<size_t>(p) * v.fb_stride;
-        for (int e = tid * nb + blockIdx.x; e < v.fb_stride; e += nt * nb) fbn[e] = face_entry(v, p, s + 1, e);
-    }
+    next_faces();
 }
 
 inline size_t pa_smem(int nr) {
