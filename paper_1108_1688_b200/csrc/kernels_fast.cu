@@ -29,6 +29,7 @@
 // Parity with the reference is 1e-10 normwise (tests/test_gpu_parity.py).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include <cooperative_groups.h>
 
@@ -1254,7 +1255,8 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     }
     const double c4 = __ldg(step_row(v, p, s) + ST_C4);
     const double2* V2 = reinterpret_cast<const double2*>(F.V + kFV * j);
-    const double2 v01 = __ldg(V2), v23 = __ldg(V2 + 1);  // (V, G2), (G5, G3V)
+    double2 v01 = __ldg(V2);
+    const double2 v23 = __ldg(V2 + 1);  // (V, G2), (G5, G3V)
     const double2* Y2 = reinterpret_cast<const double2*>(F.Y + kFY * k);
     const double2 y01 = __ldg(Y2), y23 = __ldg(Y2 + 1);  // (S6, T6), (Y, pad)
     const double vj = v01.x, yk = y23.x;
@@ -1267,7 +1269,11 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const bool vminD = dir(v, F_VMIN), vmaxD = dir(v, F_VMAX);
     const bool jlo = j == 0, jhi = j == NV - 1;
     const bool jdir = (jhi && vmaxD) || (jlo && vminD);
-    const bool slowj = (jlo || jhi) && !jdir;
+    // the degenerate j = 0 row uses the interior stencil with its missing j-1
+    // column replaced by j+1 and G2 replaced by G5: that is exactly the
+    // one-sided 2 g5 (u_{j+1} - u_j) term, and the cross term vanishes
+    const bool jdeg = jlo && !jdir;
+    if (jdeg) v01.y = v23.x;
     const bool order2y = v.y_order != 1, order2r = v.r_order != 1;
     const double* fbp = v.fb + static_cast<size_t>(p) * v.fb_stride;
     const double* fyk = fy + (kN ? 0 : nr);
@@ -1291,24 +1297,30 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     // (k-1 at tx 0, k+1 at tx 15; k+2 at k = 0 for the one-sided row)
     const bool edge = tx == 0 || (tx == 15 && !kN);
     const int eoff = tx == 0 ? (k0 ? 2 : -1) : 1;
-    if (!slowj && !jdir) {
+    // the j-1 column offset is a compile-time constant in each instantiation
+    auto prologue = [&](auto jd) {
+        constexpr int OFFM = decltype(jd)::value ? NY : -NY;
         const double* q = gptr(a - 1);
-        m0 = __ldg(q - NY); m1 = __ldg(q); m2 = __ldg(q + NY);
+        m0 = __ldg(q + OFFM); m1 = __ldg(q); m2 = __ldg(q + NY);
         q = gptr(a);
-        c0 = __ldg(q - NY); c1 = __ldg(q); c2 = __ldg(q + NY);
+        c0 = __ldg(q + OFFM); c1 = __ldg(q); c2 = __ldg(q + NY);
         if (edge) ce = __ldg(q + eoff);
         q = gptr(a + 1);
-        p0 = __ldg(q - NY); p1 = __ldg(q); p2 = __ldg(q + NY);
+        p0 = __ldg(q + OFFM); p1 = __ldg(q); p2 = __ldg(q + NY);
         if (edge) pe = __ldg(q + eoff);
 #pragma unroll
         for (int r = 0; r < kRing; ++r) {
             const double* g = gptr(a + 2 + r);
-            cp_async8s(myring_s + 8 * (r * 4 + 0), g - NY);
+            cp_async8s(myring_s + 8 * (r * 4 + 0), g + OFFM);
             cp_async8s(myring_s + 8 * (r * 4 + 1), g);
             cp_async8s(myring_s + 8 * (r * 4 + 2), g + NY);
             if (edge) cp_async8s(myring_s + 8 * (r * 4 + 3), g + eoff);
             cp_async_commit();
         }
+    };
+    if (!jdir) {
+        if (jdeg) prologue(std::true_type{});
+        else prologue(std::false_type{});
     }
     __syncthreads();  // the mbarrier is initialised
     bulk_wait(tbar_s);  // rt, fy have landed
@@ -1349,7 +1361,6 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         next_faces();
         return;
     }
-    if (slowj) cp_async_wait<0>();
 
     // row coefficients of I - th L_r at row i (g4h shared with the stencil)
     auto coeffs = [&](int i, double g1s, double g4h, double& l, double& d, double& u, double& s2) {
@@ -1391,43 +1402,8 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
     int bad_r = 0;
     bool ok = true;
-    if (slowj) {
-        // face rows j = 0 / nv-1: generic stencil per node, then the plain segment solve
-#pragma unroll
-        for (int r = 0; r < M; ++r) x[r] = explicit_slow(v, p, s, a + r, j, k);
-        double f0d = 1.0, f0u = 0.0;
-        if (a == 0) {
-            double2 r01, r23, r45, r67;
-            rtab(0, r01, r23, r45, r67);
-            double l0, d0, u0, s20, l1, d1, u1, t1;
-            coeffs(0, r01.x * vj, g4(r01, r23, r45), l0, d0, u0, s20);
-            f0d = d0;
-            f0u = u0;
-            if (s20 != 0.0) {
-                rtab(1, r01, r23, r45, r67);
-                coeffs(1, r01.x * vj, g4(r01, r23, r45), l1, d1, u1, t1);
-                if (fabs(u1) > 1e-300) {
-                    const double f = s20 / u1;
-                    f0d = fma(-f, l1, d0);
-                    f0u = fma(-f, d1, u0);
-                    x[0] = fma(-f, x[1], x[0]);
-                } else {
-                    x[0] = fma(-s20, x[2], x[0]);
-                }
-            }
-        }
-        auto row = [&](int r, double& l, double& d, double& u) {
-            if (a == 0 && r == 0) {
-                l = 0.0; d = f0d; u = f0u;
-                return;
-            }
-            double2 r01, r23, r45, r67;
-            rtab(a + r, r01, r23, r45, r67);
-            double s2;
-            coeffs(a + r, r01.x * vj, g4(r01, r23, r45), l, d, u, s2);
-        };
-        ok = seg_solve<M>(M, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
-    } else {
+    auto march = [&](auto jd) {
+        constexpr int OFFM = decltype(jd)::value ? NY : -NY;
         // window for columns j-1 (0), j (1), j+1 (2): m = row ic-1, c = ic, p = ic+1;
         // rows ic+2 .. ic+1+kRing are in flight in this thread's ring slots
         // centre moves to row a+r: row a+r+1 comes out of ring slot (r-1) % kRing,
@@ -1440,7 +1416,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             p0 = *slot(q, 0); p1 = *slot(q, 1); p2 = *slot(q, 2);
             if (edge) pe = *slot(q, 3);
             const double* g = gptr(a + r + kRing + 1);
-            cp_async8s(myring_s + 8 * (q * 4 + 0), g - NY);
+            cp_async8s(myring_s + 8 * (q * 4 + 0), g + OFFM);
             cp_async8s(myring_s + 8 * (q * 4 + 1), g);
             cp_async8s(myring_s + 8 * (q * 4 + 2), g + NY);
             if (edge) cp_async8s(myring_s + 8 * (q * 4 + 3), g + eoff);
@@ -1534,7 +1510,9 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         };
         ok = seg_solve<M>(M, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
         cp_async_wait<0>();
-    }
+    };
+    if (jdeg) march(std::true_type{});
+    else march(std::false_type{});
     if (!ok) record_pivot(st, s, 0, j * NY + k, a + bad_r);
     // reduced-system rows as [segment][field][lane]: the column walks of the
     // reduced solve (lanes = k) are bank-conflict free
@@ -1552,7 +1530,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     __syncthreads();
     const double left = (solve && sg > 0) ? E[-8 * 16 + 6 * 16] : 0.0;  // p_{s-1} = x_{a-1}
     const double right = (solve && sg < S - 1) ? E[7 * 16] : 0.0;        // q_s = x_{a+m}
-    if (kface && !slowj) {
+    if (kface) {
         // y_max / y_min Dirichlet columns (identity rows): dU0 = face(t_next) - U
         // (solver.cpp:111-116) wherever the r faces do not take precedence
         // (discretization.cpp:153-192: r_max > y_max > v_max > r_min > y_min > v_min)
