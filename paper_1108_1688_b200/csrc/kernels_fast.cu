@@ -2046,10 +2046,7 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         if (shape == 32) launch_plane<32, 32, 1, 64>(v, s, stream);
         else if (shape == 64) launch_plane<64, 64, 1, 256>(v, s, stream);
         else if (shape == 128) {
-            if (pl == 3) launch_plane<128, 128, 2, 256>(v, s, stream);
-            else if (pl == 4) launch_plane<128, 128, 2, 128, 2>(v, s, stream);
-            else if (pl == 5) launch_plane<128, 128, 4, 128, 2>(v, s, stream);
-            else if (pl == 6) launch_plane<128, 128, 2, 256, 1>(v, s, stream);
+            if (pl == 3) launch_plane<128, 128, 2, 256>(v, s, stream);  // cluster variant (diagnostic)
             else launch_plane<128, 128, 1, 256>(v, s, stream);
         } else launch_plane<256, 256, 8, 256>(v, s, stream);
         mark(2, "fx_plane_vy_update", 24.0);
