@@ -340,10 +340,7 @@ def main():
             rc = lib.hjmsv_solver_run(h)
             assert rc in (A.OK, A.DIVERGED, A.NONFINITE), lib.hjmsv_last_error()
             assert lib.hjmsv_solver_spot_prices(h, _ptr(prices)) == 0
-            off = 0
-            for q, p in enumerate(probs):
-                assert lib.hjmsv_solver_get_grid(h, q, _ptr(grids[off:off + p.size])) == 0
-                off += p.size
+            assert lib.hjmsv_solver_get_grids(h, _ptr(grids)) == 0  # every level, one copy
             lib.hjmsv_solver_destroy(h)
             el = time.perf_counter() - t0
             if it > 0:

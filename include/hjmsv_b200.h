@@ -204,6 +204,8 @@ int32_t hjmsv_solver_report(hjmsv_solver* h, int32_t problem, hjmsv_report* out)
 int32_t hjmsv_solver_dims(hjmsv_solver* h, int32_t* nr, int32_t* nv, int32_t* ny,
                           int32_t* count, int32_t* n_steps);
 int32_t hjmsv_solver_get_grid(hjmsv_solver* h, int32_t problem, double* host_out);
+/* All problems' levels in one copy: host_out[p*nr*nv*ny + idx] (batch readout). */
+int32_t hjmsv_solver_get_grids(hjmsv_solver* h, double* host_out);
 /* Injects a level (Grid3::data + Grid3::time are public, discretization.hpp:14-17). */
 int32_t hjmsv_solver_set_grid(hjmsv_solver* h, int32_t problem, const double* host_in,
                               int32_t step_index);

@@ -100,6 +100,7 @@ SIGNATURES = {
     "hjmsv_solver_report": (I32, [HP, I32, POINTER(CReport)]),
     "hjmsv_solver_dims": (I32, [HP, POINTER(I32), POINTER(I32), POINTER(I32), POINTER(I32), POINTER(I32)]),
     "hjmsv_solver_get_grid": (I32, [HP, I32, PD]),
+    "hjmsv_solver_get_grids": (I32, [HP, PD]),
     "hjmsv_solver_set_grid": (I32, [HP, I32, PD, I32]),
     "hjmsv_solver_price": (I32, [HP, I32, c_double, c_double, c_double, PD]),
     "hjmsv_solver_spot_prices": (I32, [HP, PD]),

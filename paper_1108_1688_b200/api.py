@@ -146,6 +146,12 @@ class Solver:
         _check(self.lib.hjmsv_solver_get_grid(self.h, problem, _ptr(out)))
         return out.reshape(self.nr, self.nv, self.ny)
 
+    def grids(self) -> np.ndarray:
+        """All problems' levels in one device-to-host copy, shape (P, nr, nv, ny)."""
+        out = np.empty(self.count * self.nr * self.nv * self.ny)
+        _check(self.lib.hjmsv_solver_get_grids(self.h, _ptr(out)))
+        return out.reshape(self.count, self.nr, self.nv, self.ny)
+
     def set_grid(self, problem: int, grid: np.ndarray, step_index: int):
         g = np.ascontiguousarray(grid, dtype=np.float64).reshape(-1)
         _check(self.lib.hjmsv_solver_set_grid(self.h, problem, _ptr(g), step_index))

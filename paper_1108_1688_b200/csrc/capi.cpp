@@ -69,15 +69,36 @@ int32_t guarded(F&& f) {
     }
 }
 
+// Device buffers come from the current device's stream-ordered memory pool with
+// an unbounded release threshold: a handle's arrays go back to the pool on
+// destroy and are reused by the next handle without returning memory to the
+// driver (create/destroy per pricing call stays cheap).
+void keep_pool() {
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
 template <class T>
 T* dalloc(size_t n) {
+    keep_pool();
     void* p = nullptr;
-    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    CK(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), nullptr));
+    CK(cudaStreamSynchronize(nullptr));
     return static_cast<T*>(p);
 }
 
 void dfree(void* p) {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, nullptr);
 }
 
 }  // namespace
@@ -114,6 +135,7 @@ struct hjmsv_solver {
 
     ~hjmsv_solver() {
         if (device >= 0) cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);  // buffers return to the pool only when idle
         if (graph) cudaGraphExecDestroy(graph);
         for (void* p : {(void*)U, (void*)D, (void*)C, (void*)U0, (void*)axes, (void*)steps,
                         (void*)fast, (void*)fb, (void*)pc, (void*)st, (void*)spot_idx, (void*)spot_w,
@@ -781,6 +803,16 @@ int32_t hjmsv_mc_price(const hjmsv_problem* problem, const hjmsv_mc_config* cfg,
         const double var = cfg->n_paths > 1 ? std::max(0.0, (sum_sq - n * mu * mu) / (n - 1)) : 0.0;
         *mean = mu;
         *std_error = std::sqrt(var / n);
+    });
+}
+
+int32_t hjmsv_solver_get_grids(hjmsv_solver* h, double* host_out) {
+    return guarded([&] {
+        if (!h || !host_out) throw std::invalid_argument("null argument");
+        CK(cudaSetDevice(h->device));
+        CK(cudaMemcpyAsync(host_out, h->U, sizeof(double) * h->N * h->P, cudaMemcpyDeviceToHost,
+                           h->stream));
+        CK(cudaStreamSynchronize(h->stream));
     });
 }
 

@@ -300,3 +300,12 @@ def test_custom_face_rules_two_pass(gpu, oracle, mode, case):
     g_ref, _, _, _ = oracle.run(p, cfg)
     err = B.normwise_rel(g, g_ref)
     assert err <= tol_for(mode), f"{case}: grid normwise rel err {err:.3e}"
+
+
+def test_get_grids_matches_get_grid(gpu):
+    probs = W.make_config(4, count=5, nr=16, nv=8, ny=8, steps=10)
+    with hj.Solver(probs, mode="fast") as s:
+        s.run()
+        allg = s.grids()
+        for q in range(len(probs)):
+            assert np.array_equal(allg[q], s.grid(q))
