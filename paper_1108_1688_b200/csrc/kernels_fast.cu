@@ -1177,9 +1177,11 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
 // dU0 = dt F(U) (apply_operator, discretization.cpp:302-364; Dirichlet
 // increments solver.cpp:111-116) for the row and feeds it straight into the
 // segment elimination of I - th L_r (assemble_line_r, discretization.cpp:194-230;
-// Thomas solver.cpp:22-57 by the partition method). Face rows j = 0, nv-1
-// (block-uniform) take the generic out-of-line stencil. Columns on v/y
-// Dirichlet faces (not solved, solver.cpp:127) run identity rows, so dU1 = dU0.
+// Thomas solver.cpp:22-57 by the partition method). Dirichlet v-face rows
+// (block-uniform) take a load-store-only path (dU1 = dU0 = face - U); the
+// degenerate v_min row runs the same fused march in its own instantiation.
+// Columns on y Dirichlet faces (not solved, solver.cpp:127) run identity rows,
+// so dU1 = dU0 there.
 constexpr int kRing = 4;
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -1265,7 +1267,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const bool rmaxD = dir(v, F_RMAX), rminD = dir(v, F_RMIN);
     // v-face rows (block-uniform): j = nv-1 is the v_max Dirichlet face (an early,
     // load-store-only path); j = 0 is Dirichlet (same path) or the degenerate
-    // one-sided row, which takes the generic out-of-line stencil
+    // one-sided row (below)
     const bool vminD = dir(v, F_VMIN), vmaxD = dir(v, F_VMAX);
     const bool jlo = j == 0, jhi = j == NV - 1;
     const bool jdir = (jhi && vmaxD) || (jlo && vminD);
