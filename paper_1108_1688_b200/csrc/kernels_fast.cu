@@ -1287,7 +1287,9 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     double x[M], cs[M], al[M];
     // window for columns j-1 (0), j (1), j+1 (2): m = row ic-1, c = ic, p = ic+1;
     // rows ic+2 .. ic+1+kRing are in flight in this thread's ring slots (groups 1..kRing)
-    double m0 = 0.0, m1 = 0.0, m2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, p0 = 0.0, p1 = 0.0, p2 = 0.0;
+    // row ic-1 is kept as its centre value m1 and its j+1 - j-1 difference mx (the
+    // cross term needs only that), saving two registers in the march
+    double mx = 0.0, m1 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, p0 = 0.0, p1 = 0.0, p2 = 0.0;
     double ce = 0.0, pe = 0.0;
     auto gptr = [&](int ii) { return col + static_cast<size_t>(min(max(ii, 0), nr - 1)) * SR; };
     // this thread's ring slots: 17-double stride between threads (conflict-free),
@@ -1303,7 +1305,8 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     auto prologue = [&](auto jd) {
         constexpr int OFFM = decltype(jd)::value ? NY : -NY;
         const double* q = gptr(a - 1);
-        m0 = __ldg(q + OFFM); m1 = __ldg(q); m2 = __ldg(q + NY);
+        m1 = __ldg(q);
+        mx = __ldg(q + NY) - __ldg(q + OFFM);
         q = gptr(a);
         c0 = __ldg(q + OFFM); c1 = __ldg(q); c2 = __ldg(q + NY);
         if (edge) ce = __ldg(q + eoff);
@@ -1413,7 +1416,8 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         auto shift = [&](int r) {
             const int q = (r - 1) % kRing;
             cp_async_wait<kRing - 1>();
-            m0 = c0; m1 = c1; m2 = c2;
+            mx = c2 - c0;
+            m1 = c1;
             c0 = p0; c1 = p1; c2 = p2; ce = pe;
             p0 = *slot(q, 0); p1 = *slot(q, 1); p2 = *slot(q, 2);
             if (edge) pe = *slot(q, 3);
@@ -1438,7 +1442,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         };
         // dU0 at an interior row i from a window (mm, cc, pp)
         auto stencil = [&](int i, const double2& r01, const double2& r45, const double2& r67,
-                           double g4h, double mq0, double mq1, double mq2, double cq0, double cq1,
+                           double g4h, double mqx, double mq1, double cq0, double cq1,
                            double cq2, double pq0, double pq1, double pq2, double ed) {
             const double u0 = cq1;
             double acc = -r67.x * u0;
@@ -1446,7 +1450,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             acc = fma(g4h, pq1 - mq1, acc);
             acc = fma(v01.y, (cq2 + cq0) - 2.0 * u0, acc);
             acc = fma(v23.x, cq2 - cq0, acc);
-            acc = fma(r45.y * v23.y, (pq2 - pq0) - (mq2 - mq0), acc);
+            acc = fma(r45.y * v23.y, (pq2 - pq0) - mqx, acc);
             return yterm(i, u0, acc, r67.y, ed);
         };
         auto row = [&](int r, double& l, double& d, double& u) {
@@ -1472,7 +1476,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                     double2 q01, q23, q45, q67;
                     rtab(1, q01, q23, q45, q67);
                     const double g4h1 = g4(q01, q23, q45);
-                    const double x1 = stencil(1, q01, q45, q67, g4h1, c0, c1, c2, p0, p1, p2, n0, n1, n2, pe);
+                    const double x1 = stencil(1, q01, q45, q67, g4h1, c2 - c0, c1, p0, p1, p2, n0, n1, n2, pe);
                     double d0, u0c, s20, l1, d1, u1, t1, l0;
                     coeffs(0, r01.x * vj, g4h, l0, d0, u0c, s20);
                     double f0d = d0, f0u = u0c;
@@ -1487,7 +1491,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                             cp_async_wait<kRing - 2>();
                             double2 w01, w23, w45, w67;
                             rtab(2, w01, w23, w45, w67);
-                            const double x2 = stencil(2, w01, w45, w67, g4(w01, w23, w45), p0, p1, p2, n0,
+                            const double x2 = stencil(2, w01, w45, w67, g4(w01, w23, w45), p2 - p0, p1, n0,
                                                       n1, n2, *slot(1, 0), *slot(1, 1), *slot(1, 2),
                                                       edge ? *slot(0, 3) : 0.0);
                             x[0] = fma(-s20, x2, x[0]);
@@ -1496,10 +1500,10 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                     l = 0.0; d = f0d; u = f0u;
                     return;
                 }
-                x[0] = stencil(i, r01, r45, r67, g4h, m0, m1, m2, c0, c1, c2, p0, p1, p2, ce);
+                x[0] = stencil(i, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
             } else {
                 shift(r);
-                const double xv = stencil(i, r01, r45, r67, g4h, m0, m1, m2, c0, c1, c2, p0, p1, p2, ce);
+                const double xv = stencil(i, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
                 // face plane i = nr-1: r_max is always Dirichlet and ranks first
                 x[r] = (r == M - 1 && i == nr - 1 && rmaxD) ? rmaxv - c1 : xv;
             }
