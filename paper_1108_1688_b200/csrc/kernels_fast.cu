@@ -842,106 +842,6 @@ __device__ __noinline__ double explicit_slow(const BatchView v, int p, int s, in
 // fast_step dispatches to them for the benchmark shapes and falls back to the
 // runtime-shape kernels above otherwise.
 
-// ------------------------------------------------------------ explicit, 2.5D
-// Block = 32 k x 8 j; each thread marches TI planes of its column (fully
-// unrolled) with a register window of U(i-1..i+1, j-1..j+1, k); k+-1 arrive by
-// shuffles. Loads use clamped indices (no branches); the y faces and the
-// one-sided y row are selects; face planes (i = 0, nr-1) and face rows
-// (j = 0, nv-1) take the out-of-line generic path, uniformly per warp.
-template <int NV, int NY, int TI, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_ex3(BatchView v, int s) {
-    __shared__ double rt[TI][kFR];
-    const int p = blockIdx.z;
-    DevStatus& st = v.st[p];
-    if (st.fail_step) return;
-    const int nr = v.nr;
-    const int i0 = blockIdx.y * TI;
-    const int tid = threadIdx.y * 32 + threadIdx.x;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) st.maxdelta_bits = 0ull;
-    const FT F = ftab(v, p);
-    if (tid < TI * kFR) {
-        const int ii = min(i0 + tid / kFR, nr - 1);
-        rt[tid / kFR][tid % kFR] = F.R[kFR * ii + tid % kFR];
-    }
-    constexpr int TK = NY / 32 > 0 ? NY / 32 : 1;
-    constexpr int SR = NV * NY;
-    const int jt = blockIdx.x / TK;
-    const int k = (blockIdx.x - jt * TK) * 32 + threadIdx.x;
-    const int j = jt * 8 + threadIdx.y;
-    const size_t off = static_cast<size_t>(p) * v.N;
-    __syncthreads();
-    if (j == 0 || j == NV - 1) {  // face rows: generic path (whole warp)
-#pragma unroll 1
-        for (int t = 0; t < TI; ++t) {
-            const int i = i0 + t;
-            if (i < nr)
-                v.D[off + (static_cast<size_t>(i) * NV + j) * NY + k] = explicit_slow(v, p, s, i, j, k);
-        }
-        return;
-    }
-    const double* __restrict__ col = v.U + off + j * NY + k;
-    double* __restrict__ dcol = v.D + off + j * NY + k;
-    const double* Vt = F.V + kFV * j;
-    const double* Yt = F.Y + kFY * k;
-    const double vj = Vt[FV_V], g2s = Vt[FV_G2], g5h = Vt[FV_G5], g3v = Vt[FV_G3];
-    const double yk = Yt[FY_Y], vs6 = vj * Yt[FY_S6], t6 = Yt[FY_T6];
-    const double dtm = v.pc[p].dt;
-    const double c4 = step_row(v, p, s)[ST_C4];
-    const bool k0 = k == 0, kN = k == NY - 1;
-    const bool ymaxF = kN && dir(v, F_YMAX) && !v.apply_only;
-    const bool yminF = k0 && dir(v, F_YMIN) && !v.apply_only;
-    const bool zeroF = (kN && dir(v, F_YMAX)) || (k0 && dir(v, F_YMIN));
-    const bool order2y = v.y_order != 1;
-    const double* fby = v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY + (kN ? 0 : nr);
-    auto load = [&](int ii, double& m, double& c, double& pl) {
-        const double* q = col + static_cast<size_t>(min(max(ii, 0), nr - 1)) * SR;
-        c = __ldg(q);
-        m = __ldg(q - NY);
-        pl = __ldg(q + NY);
-    };
-    double wm0, wm1, wm2, w00, w01, w02;
-    load(i0 - 1, wm0, wm1, wm2);
-    load(i0, w00, w01, w02);
-#pragma unroll
-    for (int t = 0; t < TI; ++t) {
-        const int i = i0 + t;
-        double wp0, wp1, wp2;
-        load(i + 1, wp0, wp1, wp2);
-        double kl = __shfl_up_sync(0xffffffffu, w01, 1);
-        double kr = __shfl_down_sync(0xffffffffu, w01, 1);
-        const double* q = col + static_cast<size_t>(min(i, nr - 1)) * SR;
-        if (threadIdx.x == 0 && !k0) kl = __ldg(q - 1);
-        if (threadIdx.x == 31 && !kN) kr = __ldg(q + 1);
-        const double k2 = k0 ? __ldg(q + 2) : 0.0;
-        const double fbv = (ymaxF || yminF) ? __ldg(fby + min(i, nr - 1)) : 0.0;
-        if (i < nr) {
-            double out;
-            if (i > 0 && i < nr - 1) {
-                const double* R = rt[t];
-                const double g4h = fma(c4, R[FR_G4C], fma(R[FR_G4Q], yk, fma(R[FR_G4V], vj, R[FR_G4P])));
-                const double u0 = w01;
-                double acc = -R[FR_REACT] * u0;
-                acc = fma(R[FR_G1] * vj, (wp1 + wm1) - 2.0 * u0, acc);
-                acc = fma(g4h, wp1 - wm1, acc);
-                acc = fma(g2s, (w02 + w00) - 2.0 * u0, acc);
-                acc = fma(g5h, w02 - w00, acc);
-                acc = fma(R[FR_G3] * g3v, (wp2 - wp0) - (wm2 - wm0), acc);
-                // one-sided y row at k = 0 (discretization.cpp:346-352)
-                const double yd = k0 ? (order2y ? fma(4.0, kr, -k2) - 3.0 * u0 : 2.0 * (kr - u0))
-                                     : kr - kl;
-                acc = fma(fma(R[FR_A], vs6, t6), yd, acc);
-                out = acc * dtm;
-                out = zeroF ? ((ymaxF || yminF) ? fbv - u0 : 0.0) : out;
-            } else {
-                out = explicit_slow(v, p, s, i, j, k);
-            }
-            dcol[static_cast<size_t>(i) * SR] = out;
-        }
-        wm0 = w00; wm1 = w01; wm2 = w02;
-        w00 = wp0; w01 = wp1; w02 = wp2;
-    }
-}
-
 // ------------------------------------------------------------ explicit, per node
 // Thread per node, block = 32 k x 8 j of one plane: latency is hidden by
 // occupancy (every load is independent), neighbours come from L1. Face planes
