@@ -1490,7 +1490,8 @@ struct PlaneGeom {
     static constexpr int TILE = RV * PITCH;
     static constexpr int VT = 6 * NV + 2;         // v tables: RP B E BF BB V, + the plane's 2 y-face values
     static constexpr int YT = 2 * (LY * 17);      // y tables: (S6, T6) pairs, 17-pair segments
-    static constexpr int CAR = 2 * SV * NY;       // v carries (all segments, both directions)
+    static constexpr int CP = LY * 17 + 1;        // padded carry row (same k layout as the tile rows)
+    static constexpr int CAR = 2 * SV * CP;       // v carries (all segments, both directions)
     static constexpr int EY = (NT / 32) * ((NY / 16) * (8 * (32 / (NY / 16)) + 1) + 1);  // per warp: LY x TS + 1
     static constexpr size_t SMEM = sizeof(double) * (TILE + VT + YT + CAR + EY);
     // CTAs per SM the shared memory allows, capped at 128 registers per thread
@@ -1500,6 +1501,7 @@ struct PlaneGeom {
     static_assert(32 % LY == 0 && NT % 32 == 0, "y-lines must not straddle warps");
     static_assert((RV * NY / 2) % NT == 0, "plane rows must split evenly over the block");
     __device__ static int at(int j, int k) { return j * PITCH + (k >> 4) * 17 + (k & 15); }
+    __device__ static int ci(int t, int k) { return t * CP + (k >> 4) * 17 + (k & 15); }
 };
 
 template <int NV, int NY, int CS, int NTX, int MB>
@@ -1622,7 +1624,7 @@ k_plane(BatchView v, int s) {
                     loc = fma(vtab[NV + jg], loc, vtab[jg] * tile[G::at(a + r, k)]);
                     tile[G::at(a + r, k)] = loc;
                 }
-                bcast((c * SVL + sl) * NY + k, loc);
+                bcast(G::ci(c * SVL + sl, k), loc);
                 if (bad >= 0) record_pivot(st, s, 1, i * NY + k, bad);
             }
         }
@@ -1632,8 +1634,8 @@ k_plane(BatchView v, int s) {
                 double cc = 0.0;
 #pragma unroll
                 for (int t = 0; t < SV; ++t) {
-                    const double endv = car[t * NY + k];
-                    car[t * NY + k] = cc;
+                    const double endv = car[G::ci(t, k)];
+                    car[G::ci(t, k)] = cc;
                     cc = fma(vtab[3 * NV + (t * MS + MS - 1)], cc, endv);
                 }
             }
@@ -1644,7 +1646,7 @@ k_plane(BatchView v, int s) {
                 const int k = task % NY, sl = task / NY, a = sl * MS;
                 if ((k == 0 && yminD) || (k == NY - 1 && ymaxD)) continue;
                 const int sv = c * SVL + sl;
-                const double cin = car[sv * NY + k];
+                const double cin = car[G::ci(sv, k)];
                 double xb = 0.0;
 #pragma unroll
                 for (int r = MS - 1; r >= 0; --r) {  // fix dp, local backward scan
@@ -1653,7 +1655,7 @@ k_plane(BatchView v, int s) {
                     xb = fma(vtab[2 * NV + jg], xb, dp);
                     tile[G::at(a + r, k)] = xb;
                 }
-                bcast(SV * NY + sv * NY + k, xb);
+                bcast(SV * G::CP + G::ci(sv, k), xb);
             }
         }
         cluster_sync();
@@ -1662,25 +1664,16 @@ k_plane(BatchView v, int s) {
                 double cc = 0.0;
 #pragma unroll
                 for (int t = SV - 1; t >= 0; --t) {
-                    const double firstv = car[SV * NY + t * NY + k];
-                    car[SV * NY + t * NY + k] = cc;
+                    const double firstv = car[SV * G::CP + G::ci(t, k)];
+                    car[SV * G::CP + G::ci(t, k)] = cc;
                     cc = fma(vtab[4 * NV + t * MS], cc, firstv);
                 }
             }
         }
         __syncthreads();
-        if (vwork) {
-            for (int task = tid; task < NY * SVL; task += NT) {
-                const int k = task % NY, sl = task / NY, a = sl * MS;
-                if ((k == 0 && yminD) || (k == NY - 1 && ymaxD)) continue;
-                const double cout = car[SV * NY + (c * SVL + sl) * NY + k];
-#pragma unroll
-                for (int r = 0; r < MS; ++r)
-                    tile[G::at(a + r, k)] = fma(vtab[4 * NV + j0 + a + r], cout, tile[G::at(a + r, k)]);
-            }
-        }
-        __syncthreads();
+        // the last fix-up, x_j += BB_j * carry, is applied as the y-lines read the tile
     }
+    const bool vfix = !(CS == 1 && NV <= 32) && !planeD;  // segmented v scans left a fix-up
     if (!live_p) return;  // no cluster barrier follows
 
     // ---- y-lines (rows j) + update, in rounds of NT segment tasks
@@ -1698,6 +1691,15 @@ k_plane(BatchView v, int s) {
         double x[MS], cs[MS], al[MS];
 #pragma unroll
         for (int r = 0; r < MS; ++r) x[r] = live ? tile[G::at(jl, a + r)] : 0.0;
+        if (vfix && live) {  // v-solve fix-up from the backward carries (bank-conflict-free layout)
+            const double bb = vtab[4 * NV + j];
+            const double* co = car + SV * G::CP + G::ci(j >> 4, a);
+#pragma unroll
+            for (int r = 0; r < MS; ++r) {
+                const bool skip = (r == 0 && sy == 0 && yminD) || (r == MS - 1 && sy == LY - 1 && ymaxD);
+                if (!skip) x[r] = fma(bb, co[r], x[r]);
+            }
+        }
         double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
         if (solve) {
             const double h1 = a_i * vtab[5 * NV + j];
