@@ -1483,8 +1483,10 @@ struct PlaneGeom {
     static constexpr int LY = NY / MS;            // y segments per line
     static constexpr int SV = NV / MS;            // v segments per column
     static constexpr int SVL = RV / MS;           // v segments per CTA
-    static constexpr int P0 = LY * 17;
-    static constexpr int PITCH = P0 + ((8 - (P0 % 16)) + 16) % 16;  // = 8 (mod 16)
+    // rows of 16-element segments at an 18-element stride (16-byte aligned for
+    // 128-bit accesses); PITCH = 4 (mod 16) spreads 4 consecutive rows over the banks
+    static constexpr int P0 = LY * 18;
+    static constexpr int PITCH = P0 + ((4 - (P0 % 16)) + 16) % 16;
     static constexpr int NT = NTX;
     static constexpr int YROUNDS = (RV * LY + NT - 1) / NT;
     static constexpr int TILE = RV * PITCH;
@@ -1500,7 +1502,7 @@ struct PlaneGeom {
     static_assert(RV % MS == 0 && NY % MS == 0, "segments must tile the plane");
     static_assert(32 % LY == 0 && NT % 32 == 0, "y-lines must not straddle warps");
     static_assert((RV * NY / 2) % NT == 0, "plane rows must split evenly over the block");
-    __device__ static int at(int j, int k) { return j * PITCH + (k >> 4) * 17 + (k & 15); }
+    __device__ static int at(int j, int k) { return j * PITCH + (k >> 4) * 18 + (k & 15); }
     __device__ static int ci(int t, int k) { return t * CP + (k >> 4) * 17 + (k & 15); }
 };
 
@@ -1558,8 +1560,7 @@ k_plane(BatchView v, int s) {
         for (int q = 0; q < PER; ++q) {
             const int e = q * NT + tid;
             const int j = (2 * e) / NY, k = 2 * e - j * NY;
-            tile[G::at(j, k)] = t[q].x;
-            tile[G::at(j, k + 1)] = t[q].y;
+            *reinterpret_cast<double2*>(tile + G::at(j, k)) = t[q];  // k even: 16-byte aligned
         }
         for (int e = tid; e < NV; e += NT) {
             const double* Vr = F.V + kFV * e;
@@ -1690,7 +1691,12 @@ k_plane(BatchView v, int s) {
         const bool solve = live && !planeD && !((j == 0 && vminD) || (j == NV - 1 && vmaxD));
         double x[MS], cs[MS], al[MS];
 #pragma unroll
-        for (int r = 0; r < MS; ++r) x[r] = live ? tile[G::at(jl, a + r)] : 0.0;
+        for (int q = 0; q < MS / 2; ++q) {
+            const double2 t2 = live ? *reinterpret_cast<const double2*>(tile + G::at(jl, a + 2 * q))
+                                    : make_double2(0.0, 0.0);
+            x[2 * q] = t2.x;
+            x[2 * q + 1] = t2.y;
+        }
         if (vfix && live) {  // v-solve fix-up from the backward carries (bank-conflict-free layout)
             const double bb = vtab[4 * NV + j];
             const double* co = car + SV * G::CP + G::ci(j >> 4, a);
