@@ -1684,7 +1684,8 @@ k_plane(BatchView v, int s) {
 #pragma unroll 1
     for (int h = 0; h < G::YROUNDS; ++h) {
         const int task = h * NT + tid;
-        const bool live = task < RV * LY;
+        constexpr bool ALL_LIVE = (RV * LY) % NT == 0;  // every round full: no tail lanes
+        const bool live = ALL_LIVE || task < RV * LY;
         const int jl = live ? task / LY : 0, sy = task % LY;
         const int j = j0 + jl;
         const int a = sy * MS;
@@ -1755,6 +1756,9 @@ k_plane(BatchView v, int s) {
             int bad_r = 0;
             if (!seg_solve<MS>(MS, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row))
                 record_pivot(st, s, 2, i * NV + j, a + bad_r);
+        } else {  // a line that is not solved keeps dU: zero spikes and couplings
+#pragma unroll
+            for (int r = 0; r < MS; ++r) cs[r] = al[r] = 0.0;
         }
         // reduced-system rows of the warp's lines as [segment][field][line] (padded),
         // so the per-line reduced solves (lanes = lines) are bank-conflict free
@@ -1793,14 +1797,11 @@ k_plane(BatchView v, int s) {
             const double left = (solve && sy > 0) ? e[-TS + 6 * LPW] : 0.0;
             const double right = (solve && sy < LY - 1) ? e[7 * LPW] : 0.0;
             load_u();
-            double b = bL;
+            double b = bL;  // 0 on lines that are not solved, as are cs, al, left, right
 #pragma unroll
             for (int r = MS - 1; r >= 0; --r) {
-                double dq = x[r];
-                if (solve) {
-                    if (r < MS - 1) b = -cs[r] * b;
-                    dq = fma(b, right, fma(al[r], left, x[r]));
-                }
+                if (r < MS - 1) b = -cs[r] * b;
+                const double dq = fma(b, right, fma(al[r], left, x[r]));
                 un[r] += dq;
                 x[r] = dq;
             }
