@@ -309,3 +309,48 @@ def test_get_grids_matches_get_grid(gpu):
         allg = s.grids()
         for q in range(len(probs)):
             assert np.array_equal(allg[q], s.grid(q))
+
+
+def test_collapsed_v_axis_zcb(gpu, oracle):
+    """price_zcb's collapsed mesh (singleton v axis, instruments.cpp:134-143): the
+    SPEC.md acceptance case (flat 4%, T=20, 100x40, 12 steps/yr) on the device.
+    STRICT serves collapsed axes; FAST reports UNSUPPORTED."""
+    import math
+    spot = math.log(1.04)
+    rax = AxisSpec.sinh(spot / 0.01, 0.05, 0.0, 25.0, 100)
+    yax = AxisSpec.sinh(0.0, 0.5, 0.0, 250.0, 40)
+    p = hj.ProblemSpec(r=rax, v=AxisSpec.singleton(0.0), y=yax, kappa=0.001, lam=0.15, gamma=0.9,
+                       eps=1.5, theta=0.25, rho=-0.75, maturity=20.0, flat_base=1.04, n_steps=0,
+                       time_levels=A.TIME_REFERENCE)
+    with hj.Solver([p], mode="strict") as s:
+        s.run()
+        g = s.grid(0)
+        price = s.price(0, spot / 0.01, 0.0, 0.0)  # interpolate_at on the device
+    g_ref, rep_ref, _, _ = oracle.run(p)
+    assert B.normwise_rel(g, g_ref) <= STRICT_TOL
+    assert rep_ref["n_steps"] == 240
+    assert abs(price - oracle.interpolate(p, g_ref, spot / 0.01, 0.0, 0.0)) <= 1e-12
+    assert abs(price - 1.04 ** -20) < 1e-5  # SPEC.md:525 acceptance
+    with pytest.raises(hj.Unsupported):
+        hj.Solver([p], mode="fast")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_random_shapes(gpu, oracle, mode):
+    """Seeded random grids (any nr, nv != ny, odd sizes) exercise the generic
+    FAST kernels and every STRICT path against the oracle."""
+    rng = np.random.default_rng(20261020)
+    for case in range(6):
+        nr, nv, ny = (int(rng.integers(3, 41)), int(rng.integers(3, 25)), int(rng.integers(3, 25)))
+        steps = int(rng.integers(5, 30))
+        cfg_id = int(rng.choice([0, 2, 4]))
+        p = W.make_problem(cfg_id, int(rng.integers(0, 50)), nr=nr, nv=nv, ny=ny, steps=steps)
+        grids, prices, reps, _ = solve([p], mode)
+        g_ref, rep_ref, code, _ = oracle.run(p, raise_on_error=False)
+        if code:  # the reference's scheme itself left the bound: divergence parity
+            assert reps[0]["status"] == code
+            continue
+        err = B.normwise_rel(grids[0], g_ref)
+        assert err <= tol_for(mode), f"case {case} {nr}x{nv}x{ny}: {err:.3e}"
+        p_ref = oracle.spot_price(p, g_ref)
+        assert abs(prices[0] - p_ref) <= TOL * abs(p_ref)
