@@ -1001,6 +1001,9 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
         int bad_r = 0;
         if (!seg_solve<kSegY>(kSegY, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row))
             record_pivot(st, s, 2, line, sy * kSegY + bad_r);
+    } else {  // a line that is not solved keeps dU: zero spikes and couplings
+#pragma unroll
+        for (int r = 0; r < kSegY; ++r) cs[r] = al[r] = 0.0;
     }
     double left = 0.0, right = 0.0;
     if (LY > 1) {
@@ -1021,8 +1024,8 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
             if (!reduced_solve(ew, LY, TS, bt, LPW)) record_pivot(st, s, 2, line, bt * kSegY);
         }
         __syncwarp();
-        left = sy > 0 ? e[-TS + 6 * LPW] : 0.0;
-        right = sy < LY - 1 ? e[7 * LPW] : 0.0;
+        left = (solve && sy > 0) ? e[-TS + 6 * LPW] : 0.0;
+        right = (solve && sy < LY - 1) ? e[7 * LPW] : 0.0;
     }
     // x_r, then U += dU, Dirichlet values, max|dU|, guard (solver.cpp:163-176)
     double md = 0.0;
@@ -1035,16 +1038,17 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
             un[2 * q] = t.x;
             un[2 * q + 1] = t.y;
         }
-        double b = bL;
+        double b = bL;  // 0 on lines that are not solved, as are cs, al, left, right
 #pragma unroll
         for (int r = kSegY - 1; r >= 0; --r) {
-            double dq = x[r];
-            if (solve) {
-                if (r < kSegY - 1) b = -cs[r] * b;
-                dq = fma(b, right, fma(al[r], left, x[r]));
-            }
+            if (r < kSegY - 1) b = -cs[r] * b;
+            const double dq = fma(b, right, fma(al[r], left, x[r]));
             un[r] += dq;
-            md = fmax(md, fabs(dq));
+            x[r] = dq;
+        }
+        if (v.want_md) {
+#pragma unroll
+            for (int r = 0; r < kSegY; ++r) md = fmax(md, fabs(x[r]));
         }
         if (!solve) {
 #pragma unroll
