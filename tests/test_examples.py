@@ -29,3 +29,23 @@ def test_reference_shim_matches_reference_run(gpu):
                                                       ("caplet", "strict"), ("caplet", "fast")}
     for r in rows:
         assert r["grid_rel"] <= 1e-10 and r["price_rel"] <= 1e-10, r
+
+
+CDEMO = os.path.join(ROOT, "examples", "_bin", "capi_demo")
+
+
+def test_capi_from_plain_c():
+    """include/hjmsv_b200.h compiles as C11 (-pedantic) and the host helpers run."""
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "examples"), CDEMO], check=True)
+    out = subprocess.run([CDEMO], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert json.loads(out.stdout.splitlines()[0])["abi"] >= 1
+
+
+@pytest.mark.gpu
+def test_capi_from_plain_c_solves(gpu):
+    if not os.path.exists(CDEMO):
+        pytest.skip("examples/_bin/capi_demo not built")
+    out = subprocess.run([CDEMO], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "zcb_price" in out.stdout
