@@ -71,6 +71,7 @@ struct BatchView {
     int fb_stride;        // 2ny (r faces) + 2nr (y faces) + 2 nr ny (v faces)
     double* fb_next;      // [P][fb_stride] the next step's values (filled by the last kernel of a step)
     int want_md;          // track max|dU| this step (the last step of a launched sequence)
+    int dbg;              // diagnostic switches (HJMSV_DBG; 0 in production)
 };
 
 // fast_step flags: the first step of a launched sequence fills its own face

@@ -352,6 +352,91 @@ __device__ __forceinline__ bool reduced_solve_2way(double* E, int S, int stride,
     return ok;
 }
 
+// reduced_solve_2way for a compile-time segment count, with the forward
+// recurrence in projective form. With Pp = m/d and Pq = n/d, one pair step is
+//   tA = aL m + yL d,  tB = aL n + bL d,  d' = d - aF tB,
+//   m' = tA + yF tB,   n' = bF tB
+// (den = d'/d, Qc = (aF tA + yF d)/d', Qd = bF d/d', Pp' = m'/d', Pq' = n'/d'),
+// so the loop-carried chain is a multiply and two FMAs; the reciprocal of d'
+// and the stored Qc, Qd, Pp, Pq hang off it. (m, n, d) are rescaled by exact
+// powers of two every four pairs.
+template <int S>
+__device__ __forceinline__ bool reduced_solve_2way_p(double* E, int stride, int fs, bool back,
+                                                     unsigned mask, int partner, int& bad_t) {
+    constexpr int np = S - 1;
+    constexpr int mF = (np + 1) >> 1, mB = np - mF;
+    const int fy0 = back ? 0 : 3, fa0 = back ? 2 : 4, fb0 = back ? 1 : 5;  // end row of s0
+    const int fy1 = back ? 3 : 0, fa1 = back ? 5 : 1, fb1 = back ? 4 : 2;  // first row of s1
+    const int sp = back ? 0 : 3, sq = back ? 2 : 4;                        // scratch Pp, Pq
+    const int n = back ? mB : mF;
+    double m = 0.0, nq = 0.0, d = 1.0, rd = 1.0, Pp = 0.0, Pq = 0.0;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < mF; ++k) {
+        if (k < n) {
+            double* e0 = E + (back ? S - 1 - k : k) * stride;
+            const double* e1 = E + (back ? S - 2 - k : k + 1) * stride;
+            const double aL = e0[fa0 * fs], yL = e0[fy0 * fs], bL = e0[fb0 * fs];
+            const double aF = e1[fa1 * fs], yF = e1[fy1 * fs], bF = e1[fb1 * fs];
+            const double tA = fma(aL, m, yL * d);
+            const double tB = fma(aL, nq, bL * d);
+            const double dn = fma(-aF, tB, d);
+            const double mn = fma(yF, tB, tA);
+            const double nn = bF * tB;
+            const double r = frcp(dn);
+            if (fabs(dn * rd) < 1e-300 && ok) {  // den = 1 - aF B
+                ok = false;
+                bad_t = back ? S - 2 - k : k + 1;
+            }
+            Pp = mn * r;
+            Pq = nn * r;
+            e0[6 * fs] = fma(aF, tA, yF * d) * r;  // Qc
+            e0[7 * fs] = (bF * d) * r;             // Qd
+            e0[sp * fs] = Pp;
+            e0[sq * fs] = Pq;
+            m = mn;
+            nq = nn;
+            d = dn;
+            rd = r;
+            if (k % 4 == 3) {
+                const int ex = ((__double2hiint(d) >> 20) & 0x7ff) - 1023;
+                const double sc = __hiloint2double((1023 - ex) << 20, 0);
+                const double isc = __hiloint2double((1023 + ex) << 20, 0);
+                m *= sc;
+                nq *= sc;
+                d *= sc;
+                rd *= isc;
+            }
+        }
+    }
+    // meet: p_{mF-1} = PpF + PqF q_mF (forward), q_mF = PpB + PqB p_{mF-1} (backward)
+    const double oPp = __shfl_xor_sync(mask, Pp, partner);
+    const double oPq = __shfl_xor_sync(mask, Pq, partner);
+    const double PpF = back ? oPp : Pp, PqF = back ? oPq : Pq;
+    const double PpB = back ? Pp : oPp, PqB = back ? Pq : oPq;
+    const double pm = (PpF + PqF * PpB) / (1.0 - PqF * PqB);
+    const double qm = fma(PqB, pm, PpB);
+    double qn = back ? pm : qm;
+#pragma unroll
+    for (int k = mF - 1; k >= 0; --k) {
+        if (k < n) {
+            double* e0 = E + (back ? S - 1 - k : k) * stride;
+            const double qs = fma(e0[7 * fs], qn, e0[6 * fs]);
+            const double ps = fma(e0[sq * fs], qn, e0[sp * fs]);
+            if (back) {  // reversed pair k is original pair t = S-2-k: p_t = qs, q_t = ps
+                double* et = E + (S - 2 - k) * stride;
+                et[6 * fs] = qs;
+                et[7 * fs] = ps;
+            } else {
+                e0[6 * fs] = ps;
+                e0[7 * fs] = qs;
+            }
+            qn = qs;
+        }
+    }
+    return ok;
+}
+
 // ============================================================ r-lines
 // Block = kLanesR consecutive k (same j) x S segments of M rows.
 template <int M>
@@ -784,6 +869,22 @@ __device__ __noinline__ void guard_fail(const BatchView v, int p, int s, unsigne
     }
 }
 
+// guard_finite over the M values of a segment (solver.cpp:69-77): one integer
+// max over the high words of |u| decides for all of them; only a segment with
+// a value at or above the bound's high word (or Inf/NaN) runs the exact test
+template <int M>
+__device__ __forceinline__ void guard_seg(const BatchView& v, int p, int s, unsigned long long flat0,
+                                          const double (&un)[M], double bound) {
+    unsigned hm = 0u;
+#pragma unroll
+    for (int r = 0; r < M; ++r) hm = max(hm, static_cast<unsigned>(__double2hiint(un[r])) & 0x7fffffffu);
+    if (hm >= static_cast<unsigned>(__double2hiint(bound))) {
+#pragma unroll
+        for (int r = 0; r < M; ++r)
+            if (!(fabs(un[r]) <= bound)) guard_fail(v, p, s, flat0 + r, un[r]);
+    }
+}
+
 // dU0 at a node of a face plane i, a face row j (generic stencil, one-sided rows)
 __device__ __noinline__ double explicit_slow(const BatchView v, int p, int s, int i, int j,
                                              int k) {
@@ -1016,7 +1117,7 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
             const unsigned m2 = __ballot_sync(0xffffffffu, two);
             if (two) {
                 int bt = 0;
-                if (!reduced_solve_2way(ew, LY, TS, LPW, sy == 1, m2, 1, bt))
+                if (!reduced_solve_2way_p<LY>(ew, TS, LPW, sy == 1, m2, 1, bt))
                     record_pivot(st, s, 2, line, bt * kSegY);
             }
         } else if (sy == 0 && solve) {
@@ -1062,9 +1163,7 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
             if (sy == LY - 1 && ymaxD) un[kSegY - 1] = __ldg(fby + i);
         }
         const double bound = v.pc[p].bound;
-#pragma unroll
-        for (int r = 0; r < kSegY; ++r)
-            if (!(fabs(un[r]) <= bound)) guard_fail(v, p, s, lb - off + r, un[r]);
+        guard_seg<kSegY>(v, p, s, lb - off, un, bound);
 #pragma unroll
         for (int q = 0; q < kSegY / 2; ++q) u2[q] = make_double2(un[2 * q], un[2 * q + 1]);
     }
@@ -1132,7 +1231,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     double* fy = rt + v.nr * kFR;              // [2][nr] y-face values (YMAX, YMIN)
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
-    const int fail = st.fail_step;  // checked after the prologue loads are in flight
+    const int fail = v.dbg ? 0 : st.fail_step;  // checked after the prologue loads are in flight
     const int nr = v.nr;
     const int tx = threadIdx.x, sg = threadIdx.y;
     const int tid = sg * 16 + tx;
@@ -1433,8 +1532,19 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         const unsigned mask = __ballot_sync(0xffffffffu, solve);
         if (solve) {
             int bt = 0;
-            if (!reduced_solve_2way(red + tx, S, 8 * 16, 16, sg == 1, mask, 16, bt))
-                record_pivot(st, s, 0, j * NY + k, bt * M);
+            bool rok = true;
+            if (v.dbg & 1) {  // diagnostic: uncoupled segments (wrong results, finite)
+                for (int t = 0; t < S; ++t) red[t * 128 + 96 + tx] = red[t * 128 + 112 + tx] = 0.0;
+            } else if (!(v.dbg & 2)) {
+                rok = reduced_solve_2way(red + tx, S, 8 * 16, 16, sg == 1, mask, 16, bt);
+            } else switch (S) {  // compile-time pair counts for the benchmarked shapes
+                case 4: rok = reduced_solve_2way_p<4>(red + tx, 8 * 16, 16, sg == 1, mask, 16, bt); break;
+                case 8: rok = reduced_solve_2way_p<8>(red + tx, 8 * 16, 16, sg == 1, mask, 16, bt); break;
+                case 16: rok = reduced_solve_2way_p<16>(red + tx, 8 * 16, 16, sg == 1, mask, 16, bt); break;
+                case 32: rok = reduced_solve_2way_p<32>(red + tx, 8 * 16, 16, sg == 1, mask, 16, bt); break;
+                default: rok = reduced_solve_2way(red + tx, S, 8 * 16, 16, sg == 1, mask, 16, bt);
+            }
+            if (!rok) record_pivot(st, s, 0, j * NY + k, bt * M);
         }
     }
     __syncthreads();
@@ -1529,7 +1639,7 @@ k_plane(BatchView v, int s) {
     const int p = w / nr, i = w - (w / nr) * nr;
     DevStatus& st = v.st[p];
     // a failed problem skips the work but still takes part in the cluster barriers
-    const bool live_p = st.fail_step == 0;
+    const bool live_p = v.dbg || st.fail_step == 0;
     auto cluster_sync = [] {
         if constexpr (CS > 1) cg::this_cluster().sync();
         else __syncthreads();
@@ -1549,22 +1659,39 @@ k_plane(BatchView v, int s) {
     const ProblemConst& pc = v.pc[p];
     const double th = pc.theta_dt, bound = pc.bound;
     const double a_i = __ldg(F.R + kFR * i + FR_A), react = __ldg(F.R + kFR * i + FR_REACT);
+    // single-CTA planes with 64+ rows solve the v-lines in registers: thread
+    // (kc, sl0) holds column kc's segments sl0, sl0 + SSTEP, ... (TPT of them)
+    constexpr bool REGV = CS == 1 && NV >= 64;
+    constexpr int TPT = REGV ? NY * SV / NT : 1;
+    constexpr int SSTEP = REGV ? NT / NY : 1;
+    static_assert(!REGV || (NT % NY == 0 && (NY * SV) % NT == 0), "register v-phase shape");
+    const int kc = tid % NY, sl0 = tid / NY;
+    double xv[TPT][MS];
     {  // staged even for a failed problem: the loads need not wait for the status word
         if (tid == 0) {  // U rows -> L2 early, so the update's loads hit L2
             constexpr unsigned bytes = RV * NY * sizeof(double);
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.U + pb), "r"(bytes) : "memory");
         }
-        // stage the rows of dU1: all 128-bit loads in flight, then the smem stores
-        constexpr int PER = RV * NY / 2 / NT;
-        const double2* src = reinterpret_cast<const double2*>(v.D + pb);
-        double2 t[PER];
+        if constexpr (REGV) {
+            // column segments of dU1 straight into registers (lanes = k: coalesced rows)
 #pragma unroll
-        for (int q = 0; q < PER; ++q) t[q] = __ldg(src + q * NT + tid);
+            for (int q = 0; q < TPT; ++q)
 #pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            const int e = q * NT + tid;
-            const int j = (2 * e) / NY, k = 2 * e - j * NY;
-            *reinterpret_cast<double2*>(tile + G::at(j, k)) = t[q];  // k even: 16-byte aligned
+                for (int r = 0; r < MS; ++r)
+                    xv[q][r] = __ldg(v.D + pb + static_cast<size_t>((sl0 + q * SSTEP) * MS + r) * NY + kc);
+        } else {
+            // stage the rows of dU1: all 128-bit loads in flight, then the smem stores
+            constexpr int PER = RV * NY / 2 / NT;
+            const double2* src = reinterpret_cast<const double2*>(v.D + pb);
+            double2 t[PER];
+#pragma unroll
+            for (int q = 0; q < PER; ++q) t[q] = __ldg(src + q * NT + tid);
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int e = q * NT + tid;
+                const int j = (2 * e) / NY, k = 2 * e - j * NY;
+                *reinterpret_cast<double2*>(tile + G::at(j, k)) = t[q];  // k even: 16-byte aligned
+            }
         }
         for (int e = tid; e < NV; e += NT) {
             const double* Vr = F.V + kFV * e;
@@ -1590,7 +1717,83 @@ k_plane(BatchView v, int s) {
     const bool vwork = live_p && !planeD;
 
     // ---- v-lines (columns k), skip columns on y Dirichlet faces (solver.cpp:142)
-    if (CS == 1 && NV <= 32 && !planeD) {
+    if constexpr (REGV) {
+        // the table LU's two substitutions as segmented affine scans in
+        // registers (TPT independent chains per thread), segment carries through
+        // shared memory, one store of dU2 into the tile
+        const bool colD = (kc == 0 && yminD) || (kc == NY - 1 && ymaxD);
+        const bool vs = vwork && !colD;  // block-uniform barriers below
+        if (vwork) {
+            int bad = -1;  // first singular v pivot (table NaN), warp-uniform
+#pragma unroll
+            for (int jj = 0; jj < NV; jj += 32) {
+                const unsigned m = __ballot_sync(0xffffffffu, isnan(vtab[jj + (tid & 31)]));
+                if (m && bad < 0) bad = jj + __ffs(m) - 1;
+            }
+            if (bad >= 0 && vs) record_pivot(st, s, 1, i * NY + kc, bad);
+        }
+        if (vs) {
+#pragma unroll
+            for (int q = 0; q < TPT; ++q) {
+                const int a = (sl0 + q * SSTEP) * MS;
+                double loc = 0.0;
+#pragma unroll
+                for (int r = 0; r < MS; ++r) {
+                    loc = fma(vtab[NV + a + r], loc, vtab[a + r] * xv[q][r]);
+                    xv[q][r] = loc;
+                }
+                car[G::ci(sl0 + q * SSTEP, kc)] = loc;
+            }
+        }
+        __syncthreads();
+        if (vwork && tid < NY && !colD) {  // forward carries over all segments
+            double cc = 0.0;
+#pragma unroll
+            for (int t = 0; t < SV; ++t) {
+                const double endv = car[G::ci(t, kc)];
+                car[G::ci(t, kc)] = cc;
+                cc = fma(vtab[3 * NV + (t * MS + MS - 1)], cc, endv);
+            }
+        }
+        __syncthreads();
+        if (vs) {
+#pragma unroll
+            for (int q = 0; q < TPT; ++q) {
+                const int sv = sl0 + q * SSTEP, a = sv * MS;
+                const double cin = car[G::ci(sv, kc)];
+                double xb = 0.0;
+#pragma unroll
+                for (int r = MS - 1; r >= 0; --r) {
+                    const double dp = fma(vtab[3 * NV + a + r], cin, xv[q][r]);
+                    xb = fma(vtab[2 * NV + a + r], xb, dp);
+                    xv[q][r] = xb;
+                }
+                car[SV * G::CP + G::ci(sv, kc)] = xb;
+            }
+        }
+        __syncthreads();
+        if (vwork && tid < NY && !colD) {  // backward carries from the top
+            double cc = 0.0;
+#pragma unroll
+            for (int t = SV - 1; t >= 0; --t) {
+                const double firstv = car[SV * G::CP + G::ci(t, kc)];
+                car[SV * G::CP + G::ci(t, kc)] = cc;
+                cc = fma(vtab[4 * NV + t * MS], cc, firstv);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < TPT; ++q) {
+            const int sv = sl0 + q * SSTEP, a = sv * MS;
+            const double co = vs ? car[SV * G::CP + G::ci(sv, kc)] : 0.0;
+#pragma unroll
+            for (int r = 0; r < MS; ++r) {
+                const double xq = vs ? fma(vtab[4 * NV + a + r], co, xv[q][r]) : xv[q][r];
+                tile[G::at(a + r, kc)] = xq;
+            }
+        }
+        __syncthreads();
+    } else if (CS == 1 && NV <= 32 && !planeD) {
         // short columns: one thread per column runs the table LU's two
         // substitutions as plain recurrences (no segment carries or extra
         // passes; measured faster for 32-row columns, slower for longer ones)
@@ -1678,7 +1881,7 @@ k_plane(BatchView v, int s) {
         __syncthreads();
         // the last fix-up, x_j += BB_j * carry, is applied as the y-lines read the tile
     }
-    const bool vfix = !(CS == 1 && NV <= 32) && !planeD;  // segmented v scans left a fix-up
+    const bool vfix = !REGV && !(CS == 1 && NV <= 32) && !planeD;  // segmented v scans left a fix-up
     if (!live_p) return;  // no cluster barrier follows
 
     // ---- y-lines (rows j) + update, in rounds of NT segment tasks
@@ -1782,6 +1985,10 @@ k_plane(BatchView v, int s) {
                 un[2 * q + 1] = t.y;
             }
         };
+        // one CTA per SM (the 128-wide plane) has the registers to keep U in
+        // flight during the reduced solve
+        constexpr bool early_u = G::MINB == 1;
+        if (early_u && live) load_u();
         __syncwarp();  // a line's LY segments lie in one warp
         if constexpr (LY >= 8) {
             // segment lanes 0 and 1 of each line solve its reduced system from both ends
@@ -1789,7 +1996,7 @@ k_plane(BatchView v, int s) {
             const unsigned m2 = __ballot_sync(0xffffffffu, two);
             if (two) {
                 int bt = 0;
-                if (!reduced_solve_2way(ew, LY, TS, LPW, sy == 1, m2, 1, bt))
+                if (!reduced_solve_2way_p<LY>(ew, TS, LPW, sy == 1, m2, 1, bt))
                     record_pivot(st, s, 2, i * NV + j, bt * MS);
             }
         } else if (solve && sy == 0 && LY > 1) {  // short systems: one lane (measured faster)
@@ -1800,7 +2007,7 @@ k_plane(BatchView v, int s) {
         if (live) {
             const double left = (solve && sy > 0) ? e[-TS + 6 * LPW] : 0.0;
             const double right = (solve && sy < LY - 1) ? e[7 * LPW] : 0.0;
-            load_u();
+            if (!early_u) load_u();
             double b = bL;  // 0 on lines that are not solved, as are cs, al, left, right
 #pragma unroll
             for (int r = MS - 1; r >= 0; --r) {
@@ -1820,10 +2027,7 @@ k_plane(BatchView v, int s) {
                 if (sy == 0 && yminD) un[0] = vtab[6 * NV + 1];
                 if (sy == LY - 1 && ymaxD) un[MS - 1] = vtab[6 * NV];
             }
-#pragma unroll
-            for (int r = 0; r < MS; ++r)  // guard_finite (solver.cpp:69-77)
-                if (!(fabs(un[r]) <= bound))
-                    guard_fail(v, p, s, (static_cast<size_t>(i) * NV + j) * NY + a + r, un[r]);
+            guard_seg<MS>(v, p, s, (static_cast<size_t>(i) * NV + j) * NY + a, un, bound);
 #pragma unroll
             for (int q = 0; q < MS / 2; ++q)
                 reinterpret_cast<double2*>(up)[q] = make_double2(un[2 * q], un[2 * q + 1]);
@@ -1896,6 +2100,11 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         w.fb_next = v0.fb + ((s + 1) & 1) * half;
     }
     w.want_md = (flags & STEP_LAST) ? 1 : 0;
+    static const int dbg_env = [] {
+        const char* e = std::getenv("HJMSV_DBG");
+        return e ? std::atoi(e) : 0;
+    }();
+    w.dbg = dbg_env;
     const BatchView& v = w;
     auto mark = [&](int idx, const char* name, double bytes) {
         if (launches) ++*launches;
