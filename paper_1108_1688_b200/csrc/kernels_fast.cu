@@ -437,6 +437,95 @@ __device__ __forceinline__ bool reduced_solve_2way_p(double* E, int stride, int 
     return ok;
 }
 
+// The reduced system of one line solved by L lanes at once (lane t = segment
+// t; lanes t >= S pad). The forward elimination of reduced_solve is the linear
+// recurrence (m, n, d)_t = M_t (m, n, d)_{t-1} of its projective state
+// (Pp = m/d, Pq = n/d; see reduced_solve_2way_p), with
+//   M_t = [[aL, yF' aL, yL + yF' bL], [0, bF' aL, bF' bL], [0, -aF' aL, 1 - aF' bL]]
+// (unprimed: segment t's last row, primed: segment t+1's first row). An
+// inclusive scan of the M_t over the lanes (log2 L shuffle steps, each product
+// rescaled by an exact power of two) gives every lane the state before its
+// pair; the lane then forms its own Qc, Qd, Pp, Pq (one reciprocal), and the
+// back-substitution q_t = Qc_t + Qd_t q_{t+1} is a suffix scan of affine maps.
+// Returns left = p_{t-1} = x_{a-1} and right = q_t = x_{a+m} of segment t, and
+// the pair index + 1 of a vanishing reduced pivot (0 if none) of this lane.
+// Every lane of the warp must call it (full-warp shuffles of width L).
+template <int L>
+__device__ __forceinline__ int reduced_scan(double yF, double aF, double bF, double yL, double aL,
+                                            double bL, int t, int S, double& left, double& right) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const double nyF = __shfl_down_sync(FULL, yF, 1, L);
+    const double naF = __shfl_down_sync(FULL, aF, 1, L);
+    const double nbF = __shfl_down_sync(FULL, bF, 1, L);
+    const bool pair = t < S - 1;  // pair t couples segments t and t+1
+    double ma = 1.0, b1 = 0.0, b2 = 0.0, n11 = 1.0, n12 = 0.0, n21 = 0.0, n22 = 1.0;
+    if (pair) {
+        ma = aL;
+        b1 = nyF * aL;
+        b2 = fma(nyF, bL, yL);
+        n11 = nbF * aL;
+        n12 = nbF * bL;
+        n21 = -naF * aL;
+        n22 = fma(-naF, bL, 1.0);
+    }
+#pragma unroll
+    for (int off = 1; off < L; off <<= 1) {  // X_t = M_t ... M_0
+        const double pa = __shfl_up_sync(FULL, ma, off, L);
+        const double p1 = __shfl_up_sync(FULL, b1, off, L);
+        const double p2 = __shfl_up_sync(FULL, b2, off, L);
+        const double q11 = __shfl_up_sync(FULL, n11, off, L);
+        const double q12 = __shfl_up_sync(FULL, n12, off, L);
+        const double q21 = __shfl_up_sync(FULL, n21, off, L);
+        const double q22 = __shfl_up_sync(FULL, n22, off, L);
+        if (t >= off) {
+            const double c1 = fma(ma, p1, fma(b1, q11, b2 * q21));
+            const double c2 = fma(ma, p2, fma(b1, q12, b2 * q22));
+            const double d11 = fma(n11, q11, n12 * q21);
+            const double d12 = fma(n11, q12, n12 * q22);
+            const double d21 = fma(n21, q11, n22 * q21);
+            const double d22 = fma(n21, q12, n22 * q22);
+            ma *= pa;
+            b1 = c1; b2 = c2; n11 = d11; n12 = d12; n21 = d21; n22 = d22;
+            const int ex = (__double2hiint(n22) >> 20) & 0x7ff;
+            if (ex != 0 && ex != 0x7ff) {
+                const double sc = __hiloint2double((2046 - ex) << 20, 0);  // 2^(1023 - ex)
+                ma *= sc; b1 *= sc; b2 *= sc; n11 *= sc; n12 *= sc; n21 *= sc; n22 *= sc;
+            }
+        }
+    }
+    // state before pair t: (m, n, d) = X_{t-1} (0, 0, 1)
+    double m = __shfl_up_sync(FULL, b2, 1, L);
+    double n = __shfl_up_sync(FULL, n12, 1, L);
+    double d = __shfl_up_sync(FULL, n22, 1, L);
+    if (t == 0) { m = 0.0; n = 0.0; d = 1.0; }
+    const double tA = fma(aL, m, yL * d);
+    const double tB = fma(aL, n, bL * d);
+    const double dn = fma(-naF, tB, d);
+    const double r = frcp(dn);
+    const int bad = (pair && fabs(dn) < 1e-300 * fabs(d)) ? t + 1 : 0;  // den = 1 - aF B
+    double c = 0.0, g = 0.0;
+    if (pair) {
+        c = fma(naF, tA, nyF * d) * r;  // Qc
+        g = (nbF * d) * r;              // Qd
+    }
+    const double Pp = fma(nyF, tB, tA) * r, Pq = (nbF * tB) * r;
+#pragma unroll
+    for (int off = 1; off < L; off <<= 1) {  // q_t = Qc_t + Qd_t q_{t+1}, q_{S-1} = 0
+        const double c2 = __shfl_down_sync(FULL, c, off, L);
+        const double g2 = __shfl_down_sync(FULL, g, off, L);
+        if (t + off < L) {
+            c = fma(g, c2, c);
+            g *= g2;
+        }
+    }
+    double qn = __shfl_down_sync(FULL, c, 1, L);
+    if (t + 1 >= L) qn = 0.0;
+    const double pt = fma(Pq, qn, Pp);  // p_t (pairs only)
+    right = c;
+    left = __shfl_up_sync(FULL, pt, 1, L);
+    return bad;
+}
+
 // ============================================================ r-lines
 // Block = kLanesR consecutive k (same j) x S segments of M rows.
 template <int M>
@@ -1218,15 +1307,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int NV, int NY>
+template <int NV, int NY, bool SCAN>
 __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     constexpr int M = 16;
     constexpr int SR = NV * NY;
     extern __shared__ double sm[];
     const int S = blockDim.y;
     const int nt = 16 * S;
-    double* red = sm;                          // [16][S][8] reduced-system rows
-    double* ring = red + nt * 8;               // [nt][kRing*4 + 1] window prefetch (padded)
+    double* red = sm;                          // [16][8S+9] reduced-system rows
+    double* ring = red + 16 * (8 * S + 9);     // [nt][kRing*4 + 1] window prefetch (padded)
     double* rt = ring + (kRing * 4 + 1) * nt;  // [nr][8] r-table (FastR)
     double* fy = rt + v.nr * kFR;              // [2][nr] y-face values (YMAX, YMIN)
     const int p = blockIdx.y;
@@ -1523,33 +1612,51 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     if (jdeg) march(std::true_type{});
     else march(std::false_type{});
     if (!ok) record_pivot(st, s, 0, j * NY + k, a + bad_r);
-    // reduced-system rows as [segment][field][lane]: the column walks of the
-    // reduced solve (lanes = k) are bank-conflict free
-    double* E = red + sg * 8 * 16 + tx;
-    E[0] = yF; E[16] = aF; E[32] = bF; E[48] = yL; E[64] = aL; E[80] = bL;
+    // reduced-system rows as [column][field][segment] (field stride S+1, column
+    // stride 8S+9: conflict-free for the writers, lanes = k, and for the
+    // scans, lanes = segments)
+    const int FS = S + 1, CST = 8 * S + 9;
+    double* E = red + tx * CST + sg;
+    E[0] = yF; E[FS] = aF; E[2 * FS] = bF; E[3 * FS] = yL; E[4 * FS] = aL; E[5 * FS] = bL;
     __syncthreads();
-    if (sg < 2 && S > 1) {  // warp 0: segment rows 0 (forward) and 1 (backward) of every column
-        const unsigned mask = __ballot_sync(0xffffffffu, solve);
-        if (solve) {
-            int bt = 0;
-            bool rok = true;
-            if (v.dbg & 1) {  // diagnostic: uncoupled segments (wrong results, finite)
-                for (int t = 0; t < S; ++t) red[t * 128 + 96 + tx] = red[t * 128 + 112 + tx] = 0.0;
-            } else if (!(v.dbg & 2)) {
-                rok = reduced_solve_2way(red + tx, S, 8 * 16, 16, sg == 1, mask, 16, bt);
-            } else switch (S) {  // compile-time pair counts for the benchmarked shapes
-                case 4: rok = reduced_solve_2way_p<4>(red + tx, 8 * 16, 16, sg == 1, mask, 16, bt); break;
-                case 8: rok = reduced_solve_2way_p<8>(red + tx, 8 * 16, 16, sg == 1, mask, 16, bt); break;
-                case 16: rok = reduced_solve_2way_p<16>(red + tx, 8 * 16, 16, sg == 1, mask, 16, bt); break;
-                case 32: rok = reduced_solve_2way_p<32>(red + tx, 8 * 16, 16, sg == 1, mask, 16, bt); break;
-                default: rok = reduced_solve_2way(red + tx, S, 8 * 16, 16, sg == 1, mask, 16, bt);
+    if (S > 1) {
+        if constexpr (SCAN) {
+            // every thread solves: column tid / S, segment tid % S (16 S threads)
+            const int cc = tid / S, t = tid - cc * S;
+            double* Ec = red + cc * CST + t;
+            const int kk = (blockIdx.x - j * TK) * 16 + cc;
+            const bool csolve = !(kk == NY - 1 && ymaxD) && !(j == NV - 1 && dir(v, F_VMAX)) &&
+                                !(kk == 0 && yminD) && !(j == 0 && dir(v, F_VMIN));
+            const double eyF = Ec[0], eaF = Ec[FS], ebF = Ec[2 * FS], eyL = Ec[3 * FS], eaL = Ec[4 * FS],
+                         ebL = Ec[5 * FS];
+            double lf = 0.0, rg = 0.0;
+            int bad = 0;
+            if (S == 16) bad = reduced_scan<16>(eyF, eaF, ebF, eyL, eaL, ebL, t, S, lf, rg);
+            else bad = reduced_scan<32>(eyF, eaF, ebF, eyL, eaL, ebL, t, S, lf, rg);
+            if (v.dbg & 1) lf = rg = 0.0;  // diagnostic: uncoupled segments (wrong results, finite)
+            if (csolve && bad) record_pivot(st, s, 0, j * NY + kk, bad * M);
+            Ec[6 * FS] = lf;  // x_{a-1} of segment t
+            Ec[7 * FS] = rg;  // x_{a+m} of segment t
+        } else if (sg < 2) {  // warp 0: segment rows 0 (forward) and 1 (backward) of every column
+            const unsigned mask = __ballot_sync(0xffffffffu, solve);
+            if (solve) {
+                int bt = 0;
+                if (!reduced_solve_2way(red + tx * CST, S, 1, FS, sg == 1, mask, 16, bt))
+                    record_pivot(st, s, 0, j * NY + k, bt * M);
+                __syncwarp(mask);
+                // p_t, q_t -> each segment's left (p_{t-1}) / right (q_t), as the scan leaves them
+                if (sg == 0) {
+                    for (int t = S - 1; t >= 0; --t) {
+                        double* et = red + tx * CST + t;
+                        et[6 * FS] = t > 0 ? et[-1 + 6 * FS] : 0.0;
+                    }
+                }
             }
-            if (!rok) record_pivot(st, s, 0, j * NY + k, bt * M);
         }
     }
     __syncthreads();
-    const double left = (solve && sg > 0) ? E[-8 * 16 + 6 * 16] : 0.0;  // p_{s-1} = x_{a-1}
-    const double right = (solve && sg < S - 1) ? E[7 * 16] : 0.0;        // q_s = x_{a+m}
+    const double left = (solve && sg > 0) ? E[6 * FS] : 0.0;        // x_{a-1}
+    const double right = (solve && sg < S - 1) ? E[7 * FS] : 0.0;   // x_{a+m}
     if (kface) {
         // y_max / y_min Dirichlet columns (identity rows): dU0 = face(t_next) - U
         // (solver.cpp:111-116) wherever the r faces do not take precedence
@@ -1573,7 +1680,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
 
 inline size_t pa_smem(int nr) {
     const int S = nr / 16, nt = 16 * S;
-    return sizeof(double) * (static_cast<size_t>(nt) * 8 + static_cast<size_t>(kRing * 4 + 1) * nt +
+    return sizeof(double) * (static_cast<size_t>(16) * (8 * S + 9) + static_cast<size_t>(kRing * 4 + 1) * nt +
                              static_cast<size_t>(nr) * (kFR + 2));
 }
 
@@ -1722,7 +1829,7 @@ k_plane(BatchView v, int s) {
         // registers (TPT independent chains per thread), segment carries through
         // shared memory, one store of dU2 into the tile
         const bool colD = (kc == 0 && yminD) || (kc == NY - 1 && ymaxD);
-        const bool vs = vwork && !colD;  // block-uniform barriers below
+        const bool vs = vwork && !colD && !(v.dbg & 16);  // block-uniform barriers below
         if (vwork) {
             int bad = -1;  // first singular v pivot (table NaN), warp-uniform
 #pragma unroll
@@ -1897,6 +2004,20 @@ k_plane(BatchView v, int s) {
         const int j = j0 + jl;
         const int a = sy * MS;
         const bool solve = live && !planeD && !((j == 0 && vminD) || (j == NV - 1 && vmaxD));
+        double* up = v.U + pb + static_cast<size_t>(jl) * NY + a;
+        double un[MS];
+        auto load_u = [&] {
+#pragma unroll
+            for (int q = 0; q < MS / 2; ++q) {
+                const double2 t = reinterpret_cast<const double2*>(up)[q];
+                un[2 * q] = t.x;
+                un[2 * q + 1] = t.y;
+            }
+        };
+        // one CTA per SM (the 128-wide plane) has the registers to keep U in
+        // flight through the whole segment solve
+        constexpr bool early_u = G::MINB == 1;
+        if (early_u && live) load_u();
         double x[MS], cs[MS], al[MS];
 #pragma unroll
         for (int q = 0; q < MS / 2; ++q) {
@@ -1915,7 +2036,7 @@ k_plane(BatchView v, int s) {
             }
         }
         double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
-        if (solve) {
+        if (solve && !(v.dbg & 4)) {
             const double h1 = a_i * vtab[5 * NV + j];
             double lr[MS];
             double g60 = 0.0;
@@ -1975,24 +2096,10 @@ k_plane(BatchView v, int s) {
         if (live) {
             e[0] = yF; e[LPW] = aF; e[2 * LPW] = bF; e[3 * LPW] = yL; e[4 * LPW] = aL; e[5 * LPW] = bL;
         }
-        double* up = v.U + pb + static_cast<size_t>(jl) * NY + a;
-        double un[MS];
-        auto load_u = [&] {
-#pragma unroll
-            for (int q = 0; q < MS / 2; ++q) {
-                const double2 t = reinterpret_cast<const double2*>(up)[q];
-                un[2 * q] = t.x;
-                un[2 * q + 1] = t.y;
-            }
-        };
-        // one CTA per SM (the 128-wide plane) has the registers to keep U in
-        // flight during the reduced solve
-        constexpr bool early_u = G::MINB == 1;
-        if (early_u && live) load_u();
         __syncwarp();  // a line's LY segments lie in one warp
         if constexpr (LY >= 8) {
             // segment lanes 0 and 1 of each line solve its reduced system from both ends
-            const bool two = solve && sy < 2;
+            const bool two = solve && sy < 2 && !(v.dbg & 8);
             const unsigned m2 = __ballot_sync(0xffffffffu, two);
             if (two) {
                 int bt = 0;
@@ -2027,7 +2134,7 @@ k_plane(BatchView v, int s) {
                 if (sy == 0 && yminD) un[0] = vtab[6 * NV + 1];
                 if (sy == LY - 1 && ymaxD) un[MS - 1] = vtab[6 * NV];
             }
-            guard_seg<MS>(v, p, s, (static_cast<size_t>(i) * NV + j) * NY + a, un, bound);
+            if (!(v.dbg & 32)) guard_seg<MS>(v, p, s, (static_cast<size_t>(i) * NV + j) * NY + a, un, bound);
 #pragma unroll
             for (int q = 0; q < MS / 2; ++q)
                 reinterpret_cast<double2*>(up)[q] = make_double2(un[2 * q], un[2 * q + 1]);
@@ -2138,20 +2245,32 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         const int S = v.nr / 16;
         const dim3 g(v.nv * (v.ny / 16), v.P), b(16, S);
         const size_t sm = pa_smem(v.nr);
+        // reduced systems of 16+ segments (nr >= 256) by lane scans over all
+        // warps; shorter ones by warp 0's two-ended recurrence (measured faster:
+        // the scan's registers make the march spill)
+        const bool scan = S >= 16 && (S & (S - 1)) == 0 && !(v.dbg & 2);
         static const bool attr = [] {
             const int mx = static_cast<int>(pa_smem(512));
-            cudaFuncSetAttribute(k_pa<32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_pa<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_pa<128, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_pa<256, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_pa<32, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_pa<64, 64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_pa<128, 128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_pa<128, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_pa<256, 256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_pa<256, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             return true;
         }();
         (void)attr;
         switch (shape) {
-            case 32: k_pa<32, 32><<<g, b, sm, stream>>>(v, s); break;
-            case 64: k_pa<64, 64><<<g, b, sm, stream>>>(v, s); break;
-            case 128: k_pa<128, 128><<<g, b, sm, stream>>>(v, s); break;
-            default: k_pa<256, 256><<<g, b, sm, stream>>>(v, s); break;
+            case 32: k_pa<32, 32, false><<<g, b, sm, stream>>>(v, s); break;
+            case 64: k_pa<64, 64, false><<<g, b, sm, stream>>>(v, s); break;
+            case 128:
+                if (scan) k_pa<128, 128, true><<<g, b, sm, stream>>>(v, s);
+                else k_pa<128, 128, false><<<g, b, sm, stream>>>(v, s);
+                break;
+            default:
+                if (scan) k_pa<256, 256, true><<<g, b, sm, stream>>>(v, s);
+                else k_pa<256, 256, false><<<g, b, sm, stream>>>(v, s);
+                break;
         }
         mark(0, "fx_explicit_sweep_r", 16.0);
     } else {
