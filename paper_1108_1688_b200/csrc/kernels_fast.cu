@@ -2088,32 +2088,42 @@ k_plane(BatchView v, int s) {
 #pragma unroll
             for (int r = 0; r < MS; ++r) cs[r] = al[r] = 0.0;
         }
-        // reduced-system rows of the warp's lines as [segment][field][line] (padded),
-        // so the per-line reduced solves (lanes = lines) are bank-conflict free
-        constexpr int LPW = 32 / LY, TS = 8 * LPW + 1;
-        double* ew = ey + (tid >> 5) * (LY * TS + 1) + (tid & 31) / LY;  // this line's (0, 0)
-        double* e = ew + sy * TS;
-        if (live) {
-            e[0] = yF; e[LPW] = aF; e[2 * LPW] = bF; e[3 * LPW] = yL; e[4 * LPW] = aL; e[5 * LPW] = bL;
-        }
-        __syncwarp();  // a line's LY segments lie in one warp
-        if constexpr (LY >= 8) {
-            // segment lanes 0 and 1 of each line solve its reduced system from both ends
-            const bool two = solve && sy < 2 && !(v.dbg & 8);
-            const unsigned m2 = __ballot_sync(0xffffffffu, two);
-            if (two) {
-                int bt = 0;
-                if (!reduced_solve_2way_p<LY>(ew, TS, LPW, sy == 1, m2, 1, bt))
-                    record_pivot(st, s, 2, i * NV + j, bt * MS);
+        // the line's reduced system: its LY segments are LY consecutive lanes of
+        // one warp, solved by a lane scan (shuffles only)
+        double left = 0.0, right = 0.0;
+        if constexpr (LY > 1 && LY < 8) {
+            // short systems: one lane per line through shared memory (measured
+            // faster than the scan for 2 and 4 segments), rows as
+            // [segment][field][line] (padded, bank-conflict free)
+            constexpr int LPW = 32 / LY, TS = 8 * LPW + 1;
+            double* ew = ey + (tid >> 5) * (LY * TS + 1) + (tid & 31) / LY;  // this line's (0, 0)
+            double* e = ew + sy * TS;
+            if (live) {
+                e[0] = yF; e[LPW] = aF; e[2 * LPW] = bF; e[3 * LPW] = yL; e[4 * LPW] = aL; e[5 * LPW] = bL;
             }
-        } else if (solve && sy == 0 && LY > 1) {  // short systems: one lane (measured faster)
-            int bt = 0;
-            if (!reduced_solve(ew, LY, TS, bt, LPW)) record_pivot(st, s, 2, i * NV + j, bt * MS);
+            __syncwarp();  // a line's LY segments lie in one warp
+            if (solve && sy == 0) {
+                int bt = 0;
+                if (!reduced_solve(ew, LY, TS, bt, LPW)) record_pivot(st, s, 2, i * NV + j, bt * MS);
+            }
+            __syncwarp();
+            if (solve && sy > 0) left = e[-TS + 6 * LPW];
+            if (solve && sy < LY - 1) right = e[7 * LPW];
+            __syncwarp();  // ey is reused by the next round
+        } else if constexpr (LY > 1) {
+            double lf, rg;
+            const int bt = reduced_scan<LY>(yF, aF, bF, yL, aL, bL, sy, LY, lf, rg);
+            const unsigned bm = __ballot_sync(0xffffffffu, solve && bt != 0);
+            if (solve) {
+                // the line's first vanishing reduced pivot (its lanes are g0 .. g0+LY-1)
+                const int g0 = (tid & 31) & ~(LY - 1);
+                const unsigned lm = (bm >> g0) & ((LY < 32) ? ((1u << LY) - 1u) : 0xffffffffu);
+                if (lm && sy == __ffs(lm) - 1) record_pivot(st, s, 2, i * NV + j, bt * MS);
+                if (sy > 0) left = lf;
+                if (sy < LY - 1) right = rg;
+            }
         }
-        __syncwarp();
         if (live) {
-            const double left = (solve && sy > 0) ? e[-TS + 6 * LPW] : 0.0;
-            const double right = (solve && sy < LY - 1) ? e[7 * LPW] : 0.0;
             if (!early_u) load_u();
             double b = bL;  // 0 on lines that are not solved, as are cs, al, left, right
 #pragma unroll
@@ -2139,7 +2149,6 @@ k_plane(BatchView v, int s) {
             for (int q = 0; q < MS / 2; ++q)
                 reinterpret_cast<double2*>(up)[q] = make_double2(un[2 * q], un[2 * q + 1]);
         }
-        __syncwarp();  // ey is reused by the next round
     }
     for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
     if ((tid & 31) == 0 && md > 0.0)
