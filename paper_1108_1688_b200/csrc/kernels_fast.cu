@@ -1196,20 +1196,23 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
         for (int r = 0; r < kSegY; ++r) cs[r] = al[r] = 0.0;
     }
     double left = 0.0, right = 0.0;
-    if (LY > 1) {
+    if constexpr (LY >= 8) {  // the line's LY lanes solve its reduced system by a lane scan
+        double lf, rg;
+        const int bt = reduced_scan<LY>(yF, aF, bF, yL, aL, bL, sy, LY, lf, rg);
+        const unsigned bm = __ballot_sync(0xffffffffu, solve && bt != 0);
+        if (solve) {
+            const int g0 = lane & ~(LY - 1);
+            const unsigned lm = (bm >> g0) & ((LY < 32) ? ((1u << LY) - 1u) : 0xffffffffu);
+            if (lm && sy == __ffs(lm) - 1) record_pivot(st, s, 2, line, bt * kSegY);
+            if (sy > 0) left = lf;
+            if (sy < LY - 1) right = rg;
+        }
+    } else if (LY > 1) {
         double* ew = &rsp[wid][lane / LY];
         double* e = ew + sy * TS;
         e[0] = yF; e[LPW] = aF; e[2 * LPW] = bF; e[3 * LPW] = yL; e[4 * LPW] = aL; e[5 * LPW] = bL;
         __syncwarp();
-        if constexpr (LY >= 8) {  // two-ended reduced solve by segment lanes 0 and 1
-            const bool two = solve && sy < 2;
-            const unsigned m2 = __ballot_sync(0xffffffffu, two);
-            if (two) {
-                int bt = 0;
-                if (!reduced_solve_2way_p<LY>(ew, TS, LPW, sy == 1, m2, 1, bt))
-                    record_pivot(st, s, 2, line, bt * kSegY);
-            }
-        } else if (sy == 0 && solve) {
+        if (sy == 0 && solve) {
             int bt = 0;
             if (!reduced_solve(ew, LY, TS, bt, LPW)) record_pivot(st, s, 2, line, bt * kSegY);
         }
