@@ -1716,9 +1716,12 @@ struct PlaneGeom {
     static constexpr int TILE = RV * PITCH;
     static constexpr int VT = 6 * NV + 2;         // v tables: RP B E BF BB V, + the plane's 2 y-face values
     static constexpr int YT = 2 * (LY * 17);      // y tables: (S6, T6) pairs, 17-pair segments
-    static constexpr int CP = LY * 17 + 1;        // padded carry row (same k layout as the tile rows)
-    static constexpr int CAR = 2 * SV * CP;       // v carries (all segments, both directions)
-    static constexpr int EY = (NT / 32) * ((NY / 16) * (8 * (32 / (NY / 16)) + 1) + 1);  // per warp: LY x TS + 1
+    // v-lines of 64+ rows: register scans, segment carries as [segment][k]
+    static constexpr bool REGV = NV >= 64;
+    static constexpr int CP = NY;                 // carry row
+    static constexpr int CAR = REGV ? 2 * SV * CP : 0;  // v carries (all segments, both directions)
+    // y-line reduced rows in shared memory only for lines of < 8 segments (per warp: LY x TS + 1)
+    static constexpr int EY = LY >= 8 ? 0 : (NT / 32) * ((NY / 16) * (8 * (32 / (NY / 16)) + 1) + 1);
     static constexpr size_t SMEM = sizeof(double) * (TILE + VT + YT + CAR + EY);
     // CTAs per SM the shared memory allows, capped at 128 registers per thread
     static constexpr int BY_SMEM = static_cast<int>((227 * 1024) / (SMEM + 1024));
@@ -1727,7 +1730,7 @@ struct PlaneGeom {
     static_assert(32 % LY == 0 && NT % 32 == 0, "y-lines must not straddle warps");
     static_assert((RV * NY / 2) % NT == 0, "plane rows must split evenly over the block");
     __device__ static int at(int j, int k) { return j * PITCH + (k >> 4) * 18 + (k & 15); }
-    __device__ static int ci(int t, int k) { return t * CP + (k >> 4) * 17 + (k & 15); }
+    __device__ static int ci(int t, int k) { return t * CP + k; }
 };
 
 template <int NV, int NY, int CS, int NTX, int MB>
@@ -1769,12 +1772,12 @@ k_plane(BatchView v, int s) {
     const ProblemConst& pc = v.pc[p];
     const double th = pc.theta_dt, bound = pc.bound;
     const double a_i = __ldg(F.R + kFR * i + FR_A), react = __ldg(F.R + kFR * i + FR_REACT);
-    // single-CTA planes with 64+ rows solve the v-lines in registers: thread
-    // (kc, sl0) holds column kc's segments sl0, sl0 + SSTEP, ... (TPT of them)
-    constexpr bool REGV = CS == 1 && NV >= 64;
-    constexpr int TPT = REGV ? NY * SV / NT : 1;
+    // planes with 64+ rows solve the v-lines in registers: thread (kc, sl0)
+    // holds column kc's local segments sl0, sl0 + SSTEP, ... (TPT of them)
+    constexpr bool REGV = G::REGV;
+    constexpr int TPT = REGV ? NY * SVL / NT : 1;
     constexpr int SSTEP = REGV ? NT / NY : 1;
-    static_assert(!REGV || (NT % NY == 0 && (NY * SV) % NT == 0), "register v-phase shape");
+    static_assert(!REGV || (NT % NY == 0 && (NY * SVL) % NT == 0), "register v-phase shape");
     const int kc = tid % NY, sl0 = tid / NY;
     double xv[TPT][MS];
     {  // staged even for a failed problem: the loads need not wait for the status word
@@ -1829,10 +1832,11 @@ k_plane(BatchView v, int s) {
     // ---- v-lines (columns k), skip columns on y Dirichlet faces (solver.cpp:142)
     if constexpr (REGV) {
         // the table LU's two substitutions as segmented affine scans in
-        // registers (TPT independent chains per thread), segment carries through
-        // shared memory, one store of dU2 into the tile
+        // registers (TPT independent chains per thread); segment end values go
+        // to every CTA of the cluster, each CTA runs the (short) carry chains
+        // itself; one store of dU2 into the tile
         const bool colD = (kc == 0 && yminD) || (kc == NY - 1 && ymaxD);
-        const bool vs = vwork && !colD && !(v.dbg & 16);  // block-uniform barriers below
+        const bool vs = vwork && !colD && !(v.dbg & 16);  // cluster-uniform barriers below
         if (vwork) {
             int bad = -1;  // first singular v pivot (table NaN), warp-uniform
 #pragma unroll
@@ -1840,22 +1844,22 @@ k_plane(BatchView v, int s) {
                 const unsigned m = __ballot_sync(0xffffffffu, isnan(vtab[jj + (tid & 31)]));
                 if (m && bad < 0) bad = jj + __ffs(m) - 1;
             }
-            if (bad >= 0 && vs) record_pivot(st, s, 1, i * NY + kc, bad);
+            if (bad >= 0 && vs && c == 0) record_pivot(st, s, 1, i * NY + kc, bad);
         }
         if (vs) {
 #pragma unroll
             for (int q = 0; q < TPT; ++q) {
-                const int a = (sl0 + q * SSTEP) * MS;
+                const int a = (sl0 + q * SSTEP) * MS, ag = j0 + a;
                 double loc = 0.0;
 #pragma unroll
                 for (int r = 0; r < MS; ++r) {
-                    loc = fma(vtab[NV + a + r], loc, vtab[a + r] * xv[q][r]);
+                    loc = fma(vtab[NV + ag + r], loc, vtab[ag + r] * xv[q][r]);
                     xv[q][r] = loc;
                 }
-                car[G::ci(sl0 + q * SSTEP, kc)] = loc;
+                bcast(G::ci(c * SVL + sl0 + q * SSTEP, kc), loc);
             }
         }
-        __syncthreads();
+        cluster_sync();
         if (vwork && tid < NY && !colD) {  // forward carries over all segments
             double cc = 0.0;
 #pragma unroll
@@ -1869,19 +1873,19 @@ k_plane(BatchView v, int s) {
         if (vs) {
 #pragma unroll
             for (int q = 0; q < TPT; ++q) {
-                const int sv = sl0 + q * SSTEP, a = sv * MS;
+                const int sv = c * SVL + sl0 + q * SSTEP, ag = sv * MS;
                 const double cin = car[G::ci(sv, kc)];
                 double xb = 0.0;
 #pragma unroll
                 for (int r = MS - 1; r >= 0; --r) {
-                    const double dp = fma(vtab[3 * NV + a + r], cin, xv[q][r]);
-                    xb = fma(vtab[2 * NV + a + r], xb, dp);
+                    const double dp = fma(vtab[3 * NV + ag + r], cin, xv[q][r]);
+                    xb = fma(vtab[2 * NV + ag + r], xb, dp);
                     xv[q][r] = xb;
                 }
-                car[SV * G::CP + G::ci(sv, kc)] = xb;
+                bcast(SV * G::CP + G::ci(sv, kc), xb);
             }
         }
-        __syncthreads();
+        cluster_sync();
         if (vwork && tid < NY && !colD) {  // backward carries from the top
             double cc = 0.0;
 #pragma unroll
@@ -1894,16 +1898,17 @@ k_plane(BatchView v, int s) {
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < TPT; ++q) {
-            const int sv = sl0 + q * SSTEP, a = sv * MS;
+            const int a = (sl0 + q * SSTEP) * MS, sv = c * SVL + sl0 + q * SSTEP;
             const double co = vs ? car[SV * G::CP + G::ci(sv, kc)] : 0.0;
 #pragma unroll
             for (int r = 0; r < MS; ++r) {
-                const double xq = vs ? fma(vtab[4 * NV + a + r], co, xv[q][r]) : xv[q][r];
+                const double xq = vs ? fma(vtab[4 * NV + j0 + a + r], co, xv[q][r]) : xv[q][r];
                 tile[G::at(a + r, kc)] = xq;
             }
         }
         __syncthreads();
-    } else if (CS == 1 && NV <= 32 && !planeD) {
+    } else if (!planeD) {
+        static_assert(CS == 1 && NV <= 32, "short columns run one thread per column");
         // short columns: one thread per column runs the table LU's two
         // substitutions as plain recurrences (no segment carries or extra
         // passes; measured faster for 32-row columns, slower for longer ones)
@@ -1928,70 +1933,7 @@ k_plane(BatchView v, int s) {
             }
         }
         __syncthreads();
-    } else if (!planeD) {  // uniform over the cluster
-        if (vwork) {
-            for (int task = tid; task < NY * SVL; task += NT) {
-                const int k = task % NY, sl = task / NY, a = sl * MS;
-                if ((k == 0 && yminD) || (k == NY - 1 && ymaxD)) continue;
-                double loc = 0.0;
-                int bad = -1;
-#pragma unroll
-                for (int r = 0; r < MS; ++r) {  // local forward scan
-                    const int jg = j0 + a + r;
-                    if (isnan(vtab[jg]) && bad < 0) bad = jg;  // singular v pivot (table NaN)
-                    loc = fma(vtab[NV + jg], loc, vtab[jg] * tile[G::at(a + r, k)]);
-                    tile[G::at(a + r, k)] = loc;
-                }
-                bcast(G::ci(c * SVL + sl, k), loc);
-                if (bad >= 0) record_pivot(st, s, 1, i * NY + k, bad);
-            }
-        }
-        cluster_sync();
-        if (vwork) {
-            for (int k = tid; k < NY; k += NT) {  // forward carries over all segments
-                double cc = 0.0;
-#pragma unroll
-                for (int t = 0; t < SV; ++t) {
-                    const double endv = car[G::ci(t, k)];
-                    car[G::ci(t, k)] = cc;
-                    cc = fma(vtab[3 * NV + (t * MS + MS - 1)], cc, endv);
-                }
-            }
-        }
-        __syncthreads();
-        if (vwork) {
-            for (int task = tid; task < NY * SVL; task += NT) {
-                const int k = task % NY, sl = task / NY, a = sl * MS;
-                if ((k == 0 && yminD) || (k == NY - 1 && ymaxD)) continue;
-                const int sv = c * SVL + sl;
-                const double cin = car[G::ci(sv, k)];
-                double xb = 0.0;
-#pragma unroll
-                for (int r = MS - 1; r >= 0; --r) {  // fix dp, local backward scan
-                    const int jg = j0 + a + r;
-                    const double dp = fma(vtab[3 * NV + jg], cin, tile[G::at(a + r, k)]);
-                    xb = fma(vtab[2 * NV + jg], xb, dp);
-                    tile[G::at(a + r, k)] = xb;
-                }
-                bcast(SV * G::CP + G::ci(sv, k), xb);
-            }
-        }
-        cluster_sync();
-        if (vwork) {
-            for (int k = tid; k < NY; k += NT) {  // backward carries from the top
-                double cc = 0.0;
-#pragma unroll
-                for (int t = SV - 1; t >= 0; --t) {
-                    const double firstv = car[SV * G::CP + G::ci(t, k)];
-                    car[SV * G::CP + G::ci(t, k)] = cc;
-                    cc = fma(vtab[4 * NV + t * MS], cc, firstv);
-                }
-            }
-        }
-        __syncthreads();
-        // the last fix-up, x_j += BB_j * carry, is applied as the y-lines read the tile
     }
-    const bool vfix = !REGV && !(CS == 1 && NV <= 32) && !planeD;  // segmented v scans left a fix-up
     if (!live_p) return;  // no cluster barrier follows
 
     // ---- y-lines (rows j) + update, in rounds of NT segment tasks
@@ -2028,15 +1970,6 @@ k_plane(BatchView v, int s) {
                                     : make_double2(0.0, 0.0);
             x[2 * q] = t2.x;
             x[2 * q + 1] = t2.y;
-        }
-        if (vfix && live) {  // v-solve fix-up from the backward carries (bank-conflict-free layout)
-            const double bb = vtab[4 * NV + j];
-            const double* co = car + SV * G::CP + G::ci(j >> 4, a);
-#pragma unroll
-            for (int r = 0; r < MS; ++r) {
-                const bool skip = (r == 0 && sy == 0 && yminD) || (r == MS - 1 && sy == LY - 1 && ymaxD);
-                if (!skip) x[r] = fma(bb, co[r], x[r]);
-            }
         }
         double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
         if (solve && !(v.dbg & 4)) {
@@ -2234,7 +2167,7 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
     const int tk = (v.ny + 31) / 32, tj = (v.nv + 7) / 8;
     const int shape = specialised_shape(v);
     const int pl = plane_kernels();
-    const bool plane = pl && (shape == 32 || shape == 64 || shape == 128 || (shape == 256 && pl == 3));
+    const bool plane = pl && (shape == 32 || shape == 64 || shape == 128 || shape == 256);
     static const int pa_env = [] {
         const char* e = std::getenv("HJMSV_PA");
         return e ? std::atoi(e) : 1;
@@ -2307,7 +2240,7 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         else if (shape == 128) {
             if (pl == 3) launch_plane<128, 128, 2, 256>(v, s, stream);  // cluster variant (diagnostic)
             else launch_plane<128, 128, 1, 256>(v, s, stream);
-        } else launch_plane<256, 256, 8, 256>(v, s, stream);
+        } else launch_plane<256, 256, 4, 256>(v, s, stream);
         mark(2, "fx_plane_vy_update", 24.0);
         return;
     }
