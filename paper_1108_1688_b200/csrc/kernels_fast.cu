@@ -1524,9 +1524,12 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             cp_async_commit();
         };
         // y-direction terms and the k faces (discretization.cpp:340-352)
-        auto yterm = [&](int i, double u0, double acc, double a_i, double ed) {
-            double kl = __shfl_up_sync(hmask, u0, 1, 16);
-            double kr = __shfl_down_sync(hmask, u0, 1, 16);
+        // full: every lane of the warp is here (rows r >= 1); row 0 runs the
+        // face-row code in half-warp 0 of warp 0 only, so it shuffles per half-warp
+        auto yterm = [&](bool full, double u0, double acc, double a_i, double ed) {
+            const unsigned msk = full ? 0xffffffffu : hmask;
+            double kl = __shfl_up_sync(msk, u0, 1, 16);
+            double kr = __shfl_down_sync(msk, u0, 1, 16);
             if (tx == 0 && !k0) kl = ed;
             if (tx == 15 && !kN) kr = ed;
             double yd = kr - kl;
@@ -1536,7 +1539,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             return acc * dtm;  // y-face Dirichlet columns are fixed up after the march
         };
         // dU0 at an interior row i from a window (mm, cc, pp)
-        auto stencil = [&](int i, const double2& r01, const double2& r45, const double2& r67,
+        auto stencil = [&](bool full, const double2& r01, const double2& r45, const double2& r67,
                            double g4h, double mqx, double mq1, double cq0, double cq1,
                            double cq2, double pq0, double pq1, double pq2, double ed) {
             const double u0 = cq1;
@@ -1546,7 +1549,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             acc = fma(v01.y, (cq2 + cq0) - 2.0 * u0, acc);
             acc = fma(v23.x, cq2 - cq0, acc);
             acc = fma(r45.y * v23.y, (pq2 - pq0) - mqx, acc);
-            return yterm(i, u0, acc, r67.y, ed);
+            return yterm(full, u0, acc, r67.y, ed);
         };
         auto row = [&](int r, double& l, double& d, double& u) {
             const int i = a + r;
@@ -1563,7 +1566,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                     acc = fma(g4h, order2r ? fma(4.0, p1, -n1) - 3.0 * u0 : 2.0 * (p1 - u0), acc);
                     acc = fma(v01.y, (c2 + c0) - 2.0 * u0, acc);
                     acc = fma(v23.x, c2 - c0, acc);
-                    double x0 = yterm(0, u0, acc, r67.y, ce);
+                    double x0 = yterm(false, u0, acc, r67.y, ce);
                     // r_min Dirichlet ranks below r_max / y_max / v_max (discretization.cpp:153-192)
                     if (rminD && !(kN && ymaxD)) x0 = rminv - u0;
                     x[0] = x0;
@@ -1571,7 +1574,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                     double2 q01, q23, q45, q67;
                     rtab(1, q01, q23, q45, q67);
                     const double g4h1 = g4(q01, q23, q45);
-                    const double x1 = stencil(1, q01, q45, q67, g4h1, c2 - c0, c1, p0, p1, p2, n0, n1, n2, pe);
+                    const double x1 = stencil(false, q01, q45, q67, g4h1, c2 - c0, c1, p0, p1, p2, n0, n1, n2, pe);
                     double d0, u0c, s20, l1, d1, u1, t1, l0;
                     coeffs(0, r01.x * vj, g4h, l0, d0, u0c, s20);
                     double f0d = d0, f0u = u0c;
@@ -1586,7 +1589,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                             cp_async_wait<kRing - 2>();
                             double2 w01, w23, w45, w67;
                             rtab(2, w01, w23, w45, w67);
-                            const double x2 = stencil(2, w01, w45, w67, g4(w01, w23, w45), p2 - p0, p1, n0,
+                            const double x2 = stencil(false, w01, w45, w67, g4(w01, w23, w45), p2 - p0, p1, n0,
                                                       n1, n2, *slot(1, 0), *slot(1, 1), *slot(1, 2),
                                                       edge ? *slot(0, 3) : 0.0);
                             x[0] = fma(-s20, x2, x[0]);
@@ -1595,10 +1598,10 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                     l = 0.0; d = f0d; u = f0u;
                     return;
                 }
-                x[0] = stencil(i, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
+                x[0] = stencil(false, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
             } else {
                 shift(r);
-                const double xv = stencil(i, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
+                const double xv = stencil(true, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
                 // face plane i = nr-1: r_max is always Dirichlet and ranks first
                 x[r] = (r == M - 1 && i == nr - 1 && rmaxD) ? rmaxv - c1 : xv;
             }
