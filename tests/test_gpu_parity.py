@@ -354,3 +354,50 @@ def test_random_shapes(gpu, oracle, mode):
         assert err <= tol_for(mode), f"case {case} {nr}x{nv}x{ny}: {err:.3e}"
         p_ref = oracle.spot_price(p, g_ref)
         assert abs(prices[0] - p_ref) <= TOL * abs(p_ref)
+
+
+@pytest.mark.parametrize("nr", [16, 48, 80, 208, 512])
+def test_pass_a_segment_counts(gpu, oracle, nr):
+    """Pass A with 1, 3, 5 and 13 r-segments (warp 0's two-ended recurrence on
+    the [column][field][segment] rows) and 32 segments (the lane scan over a
+    512-thread block), full marches against the oracle."""
+    p = W.make_problem(0, 3, nr=nr, nv=32, ny=32, steps=30)
+    grids, prices, _, _ = solve([p], "fast")
+    assert_parity(p, grids[0], prices[0], oracle, "fast")
+
+
+_SCHEDULE_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+import paper_1108_1688_b200 as hj
+from paper_1108_1688_b200 import workloads as W
+from oracle import bindings as B
+o = B.restatement()
+worst = 0.0
+for (nr, n, steps) in [(32, 128, 6), (32, 256, 3), (48, 64, 10)]:
+    p = W.make_problem(2, 5, nr=nr, nv=n, ny=n, steps=steps)
+    with hj.Solver([p], mode="fast") as s:
+        s.run()
+        g = s.grid(0)
+    g_ref, _, _, _ = o.run(p)
+    worst = max(worst, B.normwise_rel(g, g_ref))
+print("WORST", worst)
+"""
+
+
+@pytest.mark.parametrize("env", [{"HJMSV_PLANE": "0"}, {"HJMSV_PLANE": "0", "HJMSV_PA": "0"},
+                                 {"HJMSV_PLANE": "3"}, {"HJMSV_DBG": "2"}])
+def test_diagnostic_schedules(gpu, env):
+    """The schedules behind the diagnostic switches (split v + y kernels with the
+    lane-scan k_y3, the four-kernel schedule, the 2-CTA cluster plane, pass A's
+    two-ended recurrence at 16+ segments) stay at parity. The switches are read
+    once per process, so each runs in its own interpreter."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _SCHEDULE_SCRIPT.format(root=root)],
+                         env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    worst = float(out.stdout.split("WORST")[-1])
+    assert worst <= TOL, (env, worst)
