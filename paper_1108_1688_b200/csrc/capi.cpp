@@ -128,6 +128,7 @@ struct hjmsv_solver {
     double wall_seconds = 0.0;
     cudaGraphExec_t graph = nullptr;
     long long graph_launches = 0;
+    int full_marches = 0;      // full marches launched on this handle
     std::vector<hjmsv_report> reports;
     std::vector<std::string> messages;
     std::vector<Lowered> low;  // host tables (init freed) for readouts
@@ -600,8 +601,11 @@ int32_t hjmsv_solver_step_async(hjmsv_solver* h, int32_t steps) {
         const int count = std::min(steps, h->S - h->step);
         h->last_launches = 0;
         CK(cudaEventRecord(h->ev0, h->stream));
-        if (count > 0 && h->step == 0 && count == h->S) {
-            // the full march: one captured graph, instantiated once per handle
+        if (count > 0 && h->step == 0 && count == h->S && h->full_marches++ > 0) {
+            // a repeated full march (reset + run on the same handle): one captured
+            // graph, instantiated once per handle. The first march of a handle is
+            // launched directly: its launches overlap the kernels, while capture
+            // and instantiation (several ms for 2000 launches) would delay them all
             if (!h->graph) {
                 cudaGraph_t g = nullptr;
                 CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));

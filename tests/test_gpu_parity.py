@@ -111,6 +111,23 @@ def test_step_by_step_matches_full_march(gpu, mode):
             s.step(1)
         g1 = s.grid(0)
         s.reset()
+        s.run()      # first full march of the handle: direct launches
+        g2 = s.grid(0)
+        s.reset()
+        s.run()      # repeated full march: the captured graph
+        g3 = s.grid(0)
+    assert np.array_equal(g1, g2)
+    assert np.array_equal(g2, g3)
+
+
+def test_repeated_full_march_two_pass(gpu):
+    """The two-pass FAST schedule gives the same level from direct launches (a
+    handle's first march) and from its captured graph (later marches)."""
+    p = W.make_problem(1, 0, nr=64, nv=128, ny=128, steps=12)
+    with hj.Solver([p], mode="fast") as s:
+        s.run()
+        g1 = s.grid(0)
+        s.reset()
         s.run()
         g2 = s.grid(0)
     assert np.array_equal(g1, g2)
