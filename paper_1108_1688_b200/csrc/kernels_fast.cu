@@ -438,77 +438,81 @@ __device__ __forceinline__ bool reduced_solve_2way_p(double* E, int stride, int 
 }
 
 // The reduced system of one line solved by L lanes at once (lane t = segment
-// t; lanes t >= S pad). The forward elimination of reduced_solve is the linear
-// recurrence (m, n, d)_t = M_t (m, n, d)_{t-1} of its projective state
-// (Pp = m/d, Pq = n/d; see reduced_solve_2way_p), with
-//   M_t = [[aL, yF' aL, yL + yF' bL], [0, bF' aL, bF' bL], [0, -aF' aL, 1 - aF' bL]]
-// (unprimed: segment t's last row, primed: segment t+1's first row). An
-// inclusive scan of the M_t over the lanes (log2 L shuffle steps, each product
-// rescaled by an exact power of two) gives every lane the state before its
-// pair; the lane then forms its own Qc, Qd, Pp, Pq (one reciprocal), and the
-// back-substitution q_t = Qc_t + Qd_t q_{t+1} is a suffix scan of affine maps.
+// t; lanes t >= S pad), i.e. reduced_solve's recurrences as lane scans. With
+// unprimed fields from segment t's last row and primed ones from segment t+1's
+// first row, Pq alone obeys a Moebius recurrence,
+//   Pq_t = bF' B_t / den_t,  B_t = aL Pq_{t-1} + bL,  den_t = 1 - aF' B_t,
+// i.e. (Pq, 1) -> N_t (Pq, 1) projectively with N_t = [[bF' aL, bF' bL], [-aF' aL, 1 - aF' bL]],
+// so an inclusive scan of 2x2 products (log2 L shuffle steps, each product
+// rescaled by an exact power of two) gives every lane Pq_{t-1}; then, with
+// r = 1/den_t,
+//   Pp_t = r aL Pp_{t-1} + r (yL + yF' B_t)
+// is an affine recurrence (a scan of (alpha, beta) pairs), and the
+// back-substitution q_t = Qc_t + Qd_t q_{t+1} a suffix scan of affine maps.
 // Returns left = p_{t-1} = x_{a-1} and right = q_t = x_{a+m} of segment t, and
 // the pair index + 1 of a vanishing reduced pivot (0 if none) of this lane.
 // Every lane of the warp must call it (full-warp shuffles of width L).
 template <int L>
 __device__ __forceinline__ int reduced_scan(double yF, double aF, double bF, double yL, double aL,
-                                            double bL, int t, int S, double& left, double& right) {
+                                             double bL, int t, int S, double& left, double& right) {
     constexpr unsigned FULL = 0xffffffffu;
     const double nyF = __shfl_down_sync(FULL, yF, 1, L);
     const double naF = __shfl_down_sync(FULL, aF, 1, L);
     const double nbF = __shfl_down_sync(FULL, bF, 1, L);
     const bool pair = t < S - 1;  // pair t couples segments t and t+1
-    double ma = 1.0, b1 = 0.0, b2 = 0.0, n11 = 1.0, n12 = 0.0, n21 = 0.0, n22 = 1.0;
+    double n11 = 1.0, n12 = 0.0, n21 = 0.0, n22 = 1.0;
     if (pair) {
-        ma = aL;
-        b1 = nyF * aL;
-        b2 = fma(nyF, bL, yL);
         n11 = nbF * aL;
         n12 = nbF * bL;
         n21 = -naF * aL;
         n22 = fma(-naF, bL, 1.0);
     }
 #pragma unroll
-    for (int off = 1; off < L; off <<= 1) {  // X_t = M_t ... M_0
-        const double pa = __shfl_up_sync(FULL, ma, off, L);
-        const double p1 = __shfl_up_sync(FULL, b1, off, L);
-        const double p2 = __shfl_up_sync(FULL, b2, off, L);
+    for (int off = 1; off < L; off <<= 1) {  // N_t ... N_0
         const double q11 = __shfl_up_sync(FULL, n11, off, L);
         const double q12 = __shfl_up_sync(FULL, n12, off, L);
         const double q21 = __shfl_up_sync(FULL, n21, off, L);
         const double q22 = __shfl_up_sync(FULL, n22, off, L);
         if (t >= off) {
-            const double c1 = fma(ma, p1, fma(b1, q11, b2 * q21));
-            const double c2 = fma(ma, p2, fma(b1, q12, b2 * q22));
             const double d11 = fma(n11, q11, n12 * q21);
             const double d12 = fma(n11, q12, n12 * q22);
             const double d21 = fma(n21, q11, n22 * q21);
             const double d22 = fma(n21, q12, n22 * q22);
-            ma *= pa;
-            b1 = c1; b2 = c2; n11 = d11; n12 = d12; n21 = d21; n22 = d22;
+            n11 = d11; n12 = d12; n21 = d21; n22 = d22;
             const int ex = (__double2hiint(n22) >> 20) & 0x7ff;
             if (ex != 0 && ex != 0x7ff) {
                 const double sc = __hiloint2double((2046 - ex) << 20, 0);  // 2^(1023 - ex)
-                ma *= sc; b1 *= sc; b2 *= sc; n11 *= sc; n12 *= sc; n21 *= sc; n22 *= sc;
+                n11 *= sc; n12 *= sc; n21 *= sc; n22 *= sc;
             }
         }
     }
-    // state before pair t: (m, n, d) = X_{t-1} (0, 0, 1)
-    double m = __shfl_up_sync(FULL, b2, 1, L);
-    double n = __shfl_up_sync(FULL, n12, 1, L);
-    double d = __shfl_up_sync(FULL, n22, 1, L);
-    if (t == 0) { m = 0.0; n = 0.0; d = 1.0; }
-    const double tA = fma(aL, m, yL * d);
-    const double tB = fma(aL, n, bL * d);
-    const double dn = fma(-naF, tB, d);
-    const double r = frcp(dn);
-    const int bad = (pair && fabs(dn) < 1e-300 * fabs(d)) ? t + 1 : 0;  // den = 1 - aF B
-    double c = 0.0, g = 0.0;
-    if (pair) {
-        c = fma(naF, tA, nyF * d) * r;  // Qc
-        g = (nbF * d) * r;              // Qd
+    // Pq_{t-1} = n/d of the product up to pair t-1 (applied to (0, 1))
+    const double pn = __shfl_up_sync(FULL, n12, 1, L);
+    const double pd = __shfl_up_sync(FULL, n22, 1, L);
+    const double Pq0 = t == 0 ? 0.0 : pn * frcp(pd);
+    const double B = fma(aL, Pq0, bL);
+    const double den = fma(-naF, B, 1.0);
+    const double r = frcp(den);
+    const int bad = (pair && fabs(den) < 1e-300) ? t + 1 : 0;
+    const double Pq = pair ? B * (nbF * r) : 0.0;
+    const double Qd = pair ? nbF * r : 0.0;
+    // Pp_t = al Pp_{t-1} + be: inclusive affine scan
+    double al = pair ? r * aL : 1.0, be = pair ? r * fma(nyF, B, yL) : 0.0;
+#pragma unroll
+    for (int off = 1; off < L; off <<= 1) {
+        const double pa = __shfl_up_sync(FULL, al, off, L);
+        const double pb = __shfl_up_sync(FULL, be, off, L);
+        if (t >= off) {
+            be = fma(al, pb, be);
+            al *= pa;
+        }
     }
-    const double Pp = fma(nyF, tB, tA) * r, Pq = (nbF * tB) * r;
+    double Pp0 = __shfl_up_sync(FULL, be, 1, L);  // Pp_{t-1}
+    if (t == 0) Pp0 = 0.0;
+    const double A = fma(aL, Pp0, yL);
+    double c = pair ? fma(naF, A, nyF) * r : 0.0;  // Qc
+    double g = Qd;
+    const double Pp = pair ? be : 0.0;
 #pragma unroll
     for (int off = 1; off < L; off <<= 1) {  // q_t = Qc_t + Qd_t q_{t+1}, q_{S-1} = 0
         const double c2 = __shfl_down_sync(FULL, c, off, L);
