@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstring>
 #include <exception>
+#include <list>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -99,6 +100,113 @@ T* dalloc(size_t n) {
 
 void dfree(void* p) {
     if (p) cudaFreeAsync(p, nullptr);
+}
+
+// Process-wide pinned host staging buffers (grow-only, reused across handles):
+// descriptor uploads and large grid readouts go through them at full DMA rate
+// instead of the driver's pageable path.
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    bool busy = false;
+};
+std::mutex g_pin_mu;
+std::list<PinnedBuf>& pinned_bufs() {
+    static auto* l = new std::list<PinnedBuf>();  // process lifetime (no exit-time cudaFreeHost)
+    return *l;
+}
+
+class PinnedLease {
+  public:
+    explicit PinnedLease(size_t bytes) {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        auto& l = pinned_bufs();
+        for (auto& x : l)
+            if (!x.busy && x.n >= bytes) { b_ = &x; break; }
+        if (!b_)
+            for (auto& x : l)
+                if (!x.busy) { b_ = &x; break; }
+        if (!b_) {
+            l.emplace_back();
+            b_ = &l.back();
+        }
+        if (b_->n < bytes) {
+            if (b_->p) cudaFreeHost(b_->p);
+            b_->p = nullptr;
+            b_->n = 0;
+            const size_t want = ((bytes + (16u << 20) - 1) >> 24) << 24;  // 16 MiB granules
+            CK(cudaMallocHost(&b_->p, want));
+            b_->n = want;
+        }
+        b_->busy = true;
+    }
+    ~PinnedLease() {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        b_->busy = false;
+    }
+    PinnedLease(const PinnedLease&) = delete;
+    PinnedLease& operator=(const PinnedLease&) = delete;
+    template <class T>
+    T* as(size_t offset_bytes = 0) const {
+        return reinterpret_cast<T*>(static_cast<char*>(b_->p) + offset_bytes);
+    }
+
+  private:
+    PinnedBuf* b_ = nullptr;
+};
+
+// run f(p) for p in [0, count) on up to `workers` host threads
+template <class F>
+void parallel_for(int count, int workers, F f) {
+    workers = std::max(1, std::min(workers, count));
+    if (workers == 1) {
+        for (int p = 0; p < count; ++p) f(p);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (int w = 0; w < workers; ++w)
+        pool.emplace_back([&, w] {
+            for (int p = w; p < count; p += workers) f(p);
+        });
+    for (auto& t : pool) t.join();
+}
+
+int host_workers() { return static_cast<int>(std::max(1u, std::thread::hardware_concurrency())); }
+
+// device -> (pageable) host copy of a large readout through pinned staging:
+// the DMA of chunk k+1 overlaps the host threads' copy of chunk k
+void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    constexpr size_t CH = 16u << 20;
+    if (bytes < 2 * CH) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return;
+    }
+    PinnedLease lease(2 * CH);
+    cudaEvent_t ev[2];
+    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    const size_t nch = (bytes + CH - 1) / CH;
+    auto issue = [&](size_t k) {
+        const size_t off = k * CH, n = std::min(CH, bytes - off);
+        CK(cudaMemcpyAsync(lease.as<char>((k & 1) * CH), static_cast<const char*>(src) + off, n,
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(ev[k & 1], st));
+    };
+    const int nth = std::min(8, host_workers());
+    issue(0);
+    for (size_t k = 0; k < nch; ++k) {
+        if (k + 1 < nch) issue(k + 1);  // its buffer's previous chunk (k-1) is already copied out
+        CK(cudaEventSynchronize(ev[k & 1]));
+        const size_t off = k * CH, n = std::min(CH, bytes - off);
+        const size_t per = (n / nth + 63) & ~size_t(63);
+        parallel_for(nth, nth, [&](int t) {
+            const size_t a = std::min(n, t * per), e = std::min(n, a + per);
+            if (e > a) std::memcpy(static_cast<char*>(dst) + off + a, lease.as<char>((k & 1) * CH) + a, e - a);
+        });
+    }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
 }
 
 }  // namespace
@@ -224,9 +332,24 @@ struct StageOverride {
     bool faces = true, apply_only = false;
 };
 
+// HJMSV_TIMING=1: phase times of hjmsv_solver_create on stderr (diagnostic)
+struct PhaseTimer {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    PhaseTimer() : on(std::getenv("HJMSV_TIMING") != nullptr), t0(std::chrono::steady_clock::now()) {}
+    void mark(const char* what) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[hjmsv create] %-22s %8.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    }
+};
+
 hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
                             const hjmsv_solver_config& cfg, int device, int mode,
                             const StageOverride* ov = nullptr) {
+    PhaseTimer pt;
     if (!problems || count < 1) throw std::invalid_argument("no problems given");
     if (mode != HJMSV_MODE_STRICT && mode != HJMSV_MODE_FAST)
         throw std::invalid_argument("unknown arithmetic mode");
@@ -259,6 +382,7 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         for (auto& e : errs)
             if (e) std::rethrow_exception(e);  // the first problem's error, in input order
     }
+    pt.mark("lower");
     for (int p = 0; p < count; ++p) {
         if (ov) {  // one explicit level (t_from, dt): the douglas_step / apply_operator stages
             L[p].n_steps = 1;
@@ -302,14 +426,25 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
     h->spot_idx = dalloc<long long>(static_cast<size_t>(count) * 8);
     h->spot_w = dalloc<double>(static_cast<size_t>(count) * 8);
     h->spot_out = dalloc<double>(count);
+    pt.mark("alloc");
     std::vector<ProblemConst> pcs(count);
     h->spot_idx_host.resize(static_cast<size_t>(count) * 8);
     h->spot_w_host.resize(static_cast<size_t>(count) * 8);
     h->term_steps.resize(count);
-    std::vector<double> axes_h(static_cast<size_t>(count) * astride);
-    std::vector<double> steps_h(static_cast<size_t>(count) * h->S * kStepStride);
+    // per-problem axes and per-step tables packed into pinned staging, in parallel
+    const size_t steps_n = static_cast<size_t>(count) * h->S * kStepStride;
+    const size_t axes_n = static_cast<size_t>(count) * astride;
+    PinnedLease stage(sizeof(double) * (steps_n + axes_n));
+    double* steps_h = stage.as<double>();
+    double* axes_h = steps_h + steps_n;
+    parallel_for(count, count >= 64 ? host_workers() : 1, [&](int p) {
+        const Lowered& l = L[p];
+        std::copy(l.axes.begin(), l.axes.end(), axes_h + static_cast<size_t>(p) * astride);
+        std::copy(l.steps.begin(), l.steps.end(), steps_h + static_cast<size_t>(p) * h->S * kStepStride);
+    });
     std::vector<TermParam> term_h(count);
     std::vector<int> term_kind(count);
+    for (int p = 0; p < count; ++p) h->term_steps[p].reserve(h->S);
     for (int p = 0; p < count; ++p) {
         const Lowered& l = L[p];
         term_h[p] = l.term;
@@ -317,9 +452,6 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         if (l.term.kind == TERM_HOST)
             CK(cudaMemcpy(h->U0 + static_cast<size_t>(p) * h->N, l.init.data(),
                           sizeof(double) * h->N, cudaMemcpyHostToDevice));
-        std::copy(l.axes.begin(), l.axes.end(), axes_h.begin() + static_cast<size_t>(p) * astride);
-        std::copy(l.steps.begin(), l.steps.end(),
-                  steps_h.begin() + static_cast<size_t>(p) * h->S * kStepStride);
         pcs[p] = l.pc;
         std::copy(l.spot_idx, l.spot_idx + 8, h->spot_idx_host.begin() + p * 8);
         std::copy(l.spot_w, l.spot_w + 8, h->spot_w_host.begin() + p * 8);
@@ -328,13 +460,15 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         for (int s = 0; s < h->S; ++s)
             h->term_steps[p].push_back(l.steps[static_cast<size_t>(s) * kStepStride + ST_TNEXT]);
     }
-    CK(cudaMemcpy(h->axes, axes_h.data(), sizeof(double) * axes_h.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->steps, steps_h.data(), sizeof(double) * steps_h.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(h->axes, axes_h, sizeof(double) * axes_n, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->steps, steps_h, sizeof(double) * steps_n, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));  // the staging buffer is released with this scope
     CK(cudaMemcpy(h->pc, pcs.data(), sizeof(ProblemConst) * count, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->spot_idx, h->spot_idx_host.data(), sizeof(long long) * 8 * count,
                   cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->spot_w, h->spot_w_host.data(), sizeof(double) * 8 * count,
                   cudaMemcpyHostToDevice));
+    pt.mark("pack + H2D tables");
     BatchView& v = h->view;
     v.P = count;
     v.nr = h->nr;
@@ -372,13 +506,17 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         v.fb_stride = 2 * h->ny + 2 * h->nr + 2 * h->nr * h->ny;
         h->fb = dalloc<double>(2 * static_cast<size_t>(count) * v.fb_stride);  // two step parities
         v.fb = h->fb;
-        std::vector<double> fast_h(static_cast<size_t>(count) * v.fast_stride);
-        for (int p = 0; p < count; ++p) {
+        const size_t fast_n = static_cast<size_t>(count) * v.fast_stride;
+        PinnedLease fstage(sizeof(double) * fast_n);
+        double* fast_h = fstage.as<double>();
+        parallel_for(count, count >= 64 ? host_workers() : 1, [&](int p) {
             const std::vector<double> ft = build_fast_tables(L[p], cfg, L[p].pc.theta_dt);
-            std::copy(ft.begin(), ft.end(), fast_h.begin() + static_cast<size_t>(p) * v.fast_stride);
-        }
-        CK(cudaMemcpy(h->fast, fast_h.data(), sizeof(double) * fast_h.size(), cudaMemcpyHostToDevice));
+            std::copy(ft.begin(), ft.end(), fast_h + static_cast<size_t>(p) * v.fast_stride);
+        });
+        CK(cudaMemcpyAsync(h->fast, fast_h, sizeof(double) * fast_n, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
         fast_prepare(v, h->stream);
+        pt.mark("fast tables");
     }
     if (init_mode == INIT_DEVICE) {
         TermParam* tp = dalloc<TermParam>(count);
@@ -386,6 +524,7 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         device_terminal(v, tp, term_kind.data(), h->U0, h->stream);
         CK(cudaStreamSynchronize(h->stream));
         dfree(tp);
+        pt.mark("device terminal");
     }
     h->reports.assign(count, hjmsv_report{});
     h->messages.assign(count, std::string());
@@ -401,6 +540,7 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         l.steps.shrink_to_fit();
     }
     h->low = std::move(L);
+    pt.mark("U0 -> U, status");
     return h.release();
 }
 
@@ -687,9 +827,7 @@ int32_t hjmsv_solver_get_grid(hjmsv_solver* h, int32_t problem, double* host_out
         if (!h || !host_out) throw std::invalid_argument("null argument");
         if (problem < 0 || problem >= h->P) throw std::invalid_argument("problem index out of range");
         CK(cudaSetDevice(h->device));
-        CK(cudaMemcpyAsync(host_out, h->U + static_cast<size_t>(problem) * h->N,
-                           sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        d2h_staged(host_out, h->U + static_cast<size_t>(problem) * h->N, sizeof(double) * h->N, h->stream);
     });
 }
 
@@ -814,9 +952,7 @@ int32_t hjmsv_solver_get_grids(hjmsv_solver* h, double* host_out) {
     return guarded([&] {
         if (!h || !host_out) throw std::invalid_argument("null argument");
         CK(cudaSetDevice(h->device));
-        CK(cudaMemcpyAsync(host_out, h->U, sizeof(double) * h->N * h->P, cudaMemcpyDeviceToHost,
-                           h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        d2h_staged(host_out, h->U, sizeof(double) * h->N * h->P, h->stream);
     });
 }
 

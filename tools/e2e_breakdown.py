@@ -31,10 +31,7 @@ for it in range(3):
     lib.hjmsv_solver_synchronize(h)
     t.append(time.perf_counter())
     lib.hjmsv_solver_spot_prices(h, _ptr(prices))
-    off = 0
-    for q, p in enumerate(probs):
-        lib.hjmsv_solver_get_grid(h, q, _ptr(grids[off:off + p.size]))
-        off += p.size
+    lib.hjmsv_solver_get_grids(h, _ptr(grids))  # every level, one call
     t.append(time.perf_counter())
     lib.hjmsv_solver_destroy(h)
     t.append(time.perf_counter())
