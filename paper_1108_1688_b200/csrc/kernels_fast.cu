@@ -242,6 +242,84 @@ __device__ __forceinline__ bool seg_solve(int m, double (&x)[M], double (&cs)[M]
     return ok;
 }
 
+// seg_solve with the same arithmetic in a latency-friendlier order, for
+// segments whose rows are cheap to regenerate (row() is called twice per row):
+// (1) the pivot continuants P_r (one FMA per row on the chain), (2) all M
+// reciprocals at once (independent), (3) the y and alpha recurrences (one op
+// per row each), (4) the back-substitution. The per-row schedule of seg_solve
+// puts a reciprocal (MUFU + 4 FP64 ops) between consecutive rows; here the
+// reciprocals overlap. Results are bit-identical to seg_solve.
+template <int M, class RowFn>
+__device__ __forceinline__ bool seg_solve_ilp(double (&x)[M], double (&cs)[M], double (&al)[M],
+                                              double& yF, double& aF, double& bF, double& yL,
+                                              double& aL, double& bL, int& bad_r, RowFn row) {
+    double rp[M];  // P_r, then P_{r-1}/P_r
+    double sc7 = 1.0;
+    {
+        double pm1 = 1.0, pm2 = 0.0, uprev = 0.0;
+#pragma unroll
+        for (int r = 0; r < M; ++r) {
+            double l, d, u;
+            row(r, l, d, u);
+            const double P = r == 0 ? d : fma(d, pm1, -(l * uprev) * pm2);
+            rp[r] = P;
+            uprev = u;
+            pm2 = pm1;
+            pm1 = P;
+            if (r % 8 == 7) {  // exact power-of-two rescaling keeps P in range
+                const int e = ((__double2hiint(pm1) >> 20) & 0x7ff) - 1023;
+                const double sc = __hiloint2double((1023 - e) << 20, 0);
+                pm1 *= sc;
+                pm2 *= sc;
+                if (r == 7) sc7 = sc;
+            }
+        }
+    }
+    static_assert(M <= 16, "one rescale carried between the phases");
+    unsigned badm = 0u;
+#pragma unroll
+    for (int r = M - 1; r >= 0; --r) {  // descending: P_{r-1} is still intact
+        const double pm1 = r == 0 ? 1.0 : (r == 8 ? rp[7] * sc7 : rp[r - 1]);
+        rp[r] = pm1 * frcp(rp[r]);
+        badm |= (fabs(rp[r]) > 1e300 ? 1u : 0u) << r;  // |pivot| < 1e-300 (solver.cpp:44-52)
+    }
+    double yprev = 0.0, aprev = 0.0;
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+        double l, d, u;
+        row(r, l, d, u);
+        const bool last = r == M - 1;
+        const double lrp = l * rp[r];
+        const double c = last ? 0.0 : u * rp[r];
+        const double yy = r == 0 ? x[r] * rp[r] : fma(-lrp, yprev, x[r] * rp[r]);
+        const double aa = r == 0 ? -lrp : -lrp * aprev;
+        if (last) {
+            yL = yy;
+            aL = aa;
+            bL = -u * rp[r];
+        }
+        cs[r] = c;
+        x[r] = yy;
+        al[r] = aa;
+        yprev = yy;
+        aprev = aa;
+    }
+    double yn = yL, an = aL, bn = bL;
+#pragma unroll
+    for (int r = M - 2; r >= 0; --r) {
+        yn = fma(-cs[r], yn, x[r]);
+        an = fma(-cs[r], an, al[r]);
+        bn = -cs[r] * bn;
+        x[r] = yn;
+        al[r] = an;
+    }
+    yF = yn;
+    aF = an;
+    bF = bn;
+    bad_r = badm ? __ffs(badm) - 1 : 0;
+    return badm == 0u;
+}
+
 // Reduced system of a line with S segments, unknowns p_t = x_last(t) and
 // q_t = x_first(t+1), t = 0..S-2:
 //   p_t = yL_t + aL_t p_{t-1} + bL_t q_t,   q_t = yF_{t+1} + aF_{t+1} p_t + bF_{t+1} q_{t+1}
@@ -2025,8 +2103,11 @@ k_plane(BatchView v, int s) {
                 }
             };
             int bad_r = 0;
-            if (!seg_solve<MS>(MS, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row))
-                record_pivot(st, s, 2, i * NV + j, a + bad_r);
+            // phase-ordered solve where the registers allow it (one CTA per SM)
+            bool sok;
+            if constexpr (G::MINB == 1) sok = seg_solve_ilp<MS>(x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
+            else sok = seg_solve<MS>(MS, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
+            if (!sok) record_pivot(st, s, 2, i * NV + j, a + bad_r);
         } else {  // a line that is not solved keeps dU: zero spikes and couplings
 #pragma unroll
             for (int r = 0; r < MS; ++r) cs[r] = al[r] = 0.0;
