@@ -1359,7 +1359,7 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
 // degenerate v_min row runs the same fused march in its own instantiation.
 // Columns on y Dirichlet faces (not solved, solver.cpp:127) run identity rows,
 // so dU1 = dU0 there.
-constexpr int kRing = 4;
+constexpr int kRing = 3;
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
