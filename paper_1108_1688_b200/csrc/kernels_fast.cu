@@ -320,6 +320,125 @@ __device__ __forceinline__ bool seg_solve_ilp(double (&x)[M], double (&cs)[M], d
     return badm == 0u;
 }
 
+// The segment solve of seg_solve by a twisted factorisation: rows 0..K-1 are
+// eliminated from the top (LU) and rows M-1..K+1 from the bottom (UL) at the
+// same time, and the two sweeps meet at row K = M/2, so each thread runs two
+// independent chains of M/2 rows instead of one of M (the same three arrays:
+// the top half keeps (c', y', alpha'), the bottom half (e', y'', beta'')).
+// The right-hand side -l_0 e_0 (alpha) only enters the top sweep and
+// -u_{M-1} e_{M-1} (beta) only the bottom one; pivots are continuant ratios in
+// both directions (P_r = d_r P_{r-1} - l_r u_{r-1} P_{r-2} from the top,
+// Q_r = d_r Q_{r+1} - u_r l_{r+1} Q_{r+2} from the bottom). On exit x[] = y,
+// al[] = alpha, cs[] = beta (the right spike; callers use it directly) and the
+// end-row values are set. Only the elimination order differs from seg_solve.
+template <int M, class RowFn>
+__device__ __forceinline__ bool seg_solve_tw(double (&x)[M], double (&cs)[M], double (&al)[M],
+                                             double& yF, double& aF, double& bF, double& yL,
+                                             double& aL, double& bL, int& bad_r, RowFn row) {
+    static_assert(M >= 4 && M % 2 == 0, "twisted segment");
+    constexpr int K = M / 2;
+    unsigned badm = 0u;
+    // top sweep, rows 0..K-1: cs = c' = u/piv, x = y', al = alpha'
+    // bottom sweep, rows M-1..K+1: cs = e' = l/piv', x = y'', al = beta''
+    double pm1 = 1.0, pm2 = 0.0, uprev = 0.0, yprev = 0.0, aprev = 0.0;
+    double qm1 = 1.0, qm2 = 0.0, lnext = 0.0, ynext = 0.0, bnext = 0.0;
+    double lK = 0.0, dK = 1.0, uK = 0.0;
+#pragma unroll
+    for (int h = 0; h < K; ++h) {
+        {  // top row r = h
+            const int r = h;
+            double l, d, u;
+            row(r, l, d, u);
+            const double P = r == 0 ? d : fma(d, pm1, -(l * uprev) * pm2);
+            const double rp = pm1 * frcp(P);  // 1/piv_r
+            badm |= (fabs(rp) > 1e300 ? 1u : 0u) << r;
+            const double lrp = l * rp;
+            cs[r] = u * rp;
+            x[r] = r == 0 ? x[r] * rp : fma(-lrp, yprev, x[r] * rp);
+            al[r] = r == 0 ? -lrp : -lrp * aprev;
+            yprev = x[r];
+            aprev = al[r];
+            uprev = u;
+            pm2 = pm1;
+            pm1 = P;
+            if (r % 8 == 7) {
+                const int e = ((__double2hiint(pm1) >> 20) & 0x7ff) - 1023;
+                const double sc = __hiloint2double((1023 - e) << 20, 0);
+                pm1 *= sc;
+                pm2 *= sc;
+            }
+        }
+        if (M - 1 - h > K) {  // bottom row r = M-1-h
+            const int r = M - 1 - h;
+            double l, d, u;
+            row(r, l, d, u);
+            const double Q = h == 0 ? d : fma(d, qm1, -(u * lnext) * qm2);
+            const double rq = qm1 * frcp(Q);  // 1/piv'_r
+            badm |= (fabs(rq) > 1e300 ? 1u : 0u) << r;
+            const double urq = u * rq;
+            cs[r] = l * rq;
+            x[r] = h == 0 ? x[r] * rq : fma(-urq, ynext, x[r] * rq);
+            al[r] = h == 0 ? -urq : -urq * bnext;
+            ynext = x[r];
+            bnext = al[r];
+            lnext = l;
+            qm2 = qm1;
+            qm1 = Q;
+            if (h % 8 == 7) {
+                const int e = ((__double2hiint(qm1) >> 20) & 0x7ff) - 1023;
+                const double sc = __hiloint2double((1023 - e) << 20, 0);
+                qm1 *= sc;
+                qm2 *= sc;
+            }
+        }
+    }
+    row(K, lK, dK, uK);
+    // middle row K: both sweeps meet
+    const double cK1 = cs[K - 1], eK1 = cs[K + 1];
+    const double piv = fma(-lK, cK1, fma(-uK, eK1, dK));
+    const double rk = frcp(piv);
+    badm |= (fabs(rk) > 1e300 ? 1u : 0u) << K;
+    const double yK = fma(-lK, x[K - 1], fma(-uK, x[K + 1], x[K])) * rk;
+    const double aK = -lK * al[K - 1] * rk;
+    const double bK = -uK * al[K + 1] * rk;
+    x[K] = yK;
+    al[K] = aK;
+    cs[K] = bK;
+    // outward back-substitution: upward rows K-1..0 and downward rows K+1..M-1
+    double yu = yK, au = aK, bu = bK, yd = yK, ad = aK, bd = bK;
+#pragma unroll
+    for (int h = 1; h <= K; ++h) {
+        {
+            const int r = K - h;  // x_r = y'_r - c'_r x_{r+1}
+            const double c = cs[r];
+            yu = fma(-c, yu, x[r]);
+            au = fma(-c, au, al[r]);
+            bu = -c * bu;
+            x[r] = yu;
+            al[r] = au;
+            cs[r] = bu;
+        }
+        if (K + h < M) {
+            const int r = K + h;  // x_r = y''_r - e'_r x_{r-1}
+            const double e = cs[r];
+            yd = fma(-e, yd, x[r]);
+            bd = fma(-e, bd, al[r]);
+            ad = -e * ad;
+            x[r] = yd;
+            al[r] = ad;
+            cs[r] = bd;
+        }
+    }
+    yF = x[0];
+    aF = al[0];
+    bF = cs[0];
+    yL = x[M - 1];
+    aL = al[M - 1];
+    bL = cs[M - 1];
+    bad_r = badm ? __ffs(badm) - 1 : 0;
+    return badm == 0u;
+}
+
 // Reduced system of a line with S segments, unknowns p_t = x_last(t) and
 // q_t = x_first(t+1), t = 0..S-2:
 //   p_t = yL_t + aL_t p_{t-1} + bL_t q_t,   q_t = yF_{t+1} + aF_{t+1} p_t + bF_{t+1} q_{t+1}
@@ -2044,10 +2163,22 @@ k_plane(BatchView v, int s) {
                 un[2 * q + 1] = t.y;
             }
         };
-        // one CTA per SM (the 128-wide plane) has the registers to keep U in
-        // flight through the whole segment solve
+        // one CTA per SM (the 128- and 256-wide planes): the warp's rows of U
+        // (32/LY lines x NY = 512 doubles, contiguous) move as coalesced 128-bit
+        // chunks (lane l holds elements 64q + 2l) and are exchanged with the
+        // lanes that own them through the warp's tile rows, which are free once
+        // every lane has read its x; loads are in flight through the solve
         constexpr bool early_u = G::MINB == 1;
-        if (early_u && live) load_u();
+        constexpr int WROWS = 32 / LY;
+        static_assert(!early_u || (WROWS * NY == 512 && ALL_LIVE), "staged U: 512 doubles per warp");
+        const int jw = jl & ~(WROWS - 1);  // the warp's first row
+        const int ln = tid & 31;
+        double2 us[early_u ? 8 : 1];
+        if constexpr (early_u) {
+            const double2* gw = reinterpret_cast<const double2*>(v.U + pb + static_cast<size_t>(jw) * NY);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) us[q] = gw[q * 32 + ln];
+        }
         double x[MS], cs[MS], al[MS];
 #pragma unroll
         for (int q = 0; q < MS / 2; ++q) {
@@ -2105,7 +2236,7 @@ k_plane(BatchView v, int s) {
             int bad_r = 0;
             // phase-ordered solve where the registers allow it (one CTA per SM)
             bool sok;
-            if constexpr (G::MINB == 1) sok = seg_solve_ilp<MS>(x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
+            if constexpr (G::MINB == 1) sok = seg_solve_tw<MS>(x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
             else sok = seg_solve<MS>(MS, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
             if (!sok) record_pivot(st, s, 2, i * NV + j, a + bad_r);
         } else {  // a line that is not solved keeps dU: zero spikes and couplings
@@ -2148,11 +2279,28 @@ k_plane(BatchView v, int s) {
             }
         }
         if (live) {
-            if (!early_u) load_u();
+            if constexpr (early_u) {
+                __syncwarp();  // every lane has read its x from the warp's tile rows
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int e = q * 64 + 2 * ln;
+                    *reinterpret_cast<double2*>(tile + G::at(jw + e / NY, e % NY)) = us[q];
+                }
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < MS / 2; ++q) {
+                    const double2 t = *reinterpret_cast<const double2*>(tile + G::at(jl, a + 2 * q));
+                    un[2 * q] = t.x;
+                    un[2 * q + 1] = t.y;
+                }
+            } else {
+                load_u();
+            }
             double b = bL;  // 0 on lines that are not solved, as are cs, al, left, right
 #pragma unroll
             for (int r = MS - 1; r >= 0; --r) {
-                if (r < MS - 1) b = -cs[r] * b;
+                if constexpr (G::MINB == 1) b = cs[r];  // the twisted solve left beta itself
+                else if (r < MS - 1) b = -cs[r] * b;
                 const double dq = fma(b, right, fma(al[r], left, x[r]));
                 un[r] += dq;
                 x[r] = dq;
@@ -2169,9 +2317,22 @@ k_plane(BatchView v, int s) {
                 if (sy == LY - 1 && ymaxD) un[MS - 1] = vtab[6 * NV];
             }
             if (!(v.dbg & 32)) guard_seg<MS>(v, p, s, (static_cast<size_t>(i) * NV + j) * NY + a, un, bound);
+            if constexpr (early_u) {  // back through the tile rows, out as coalesced chunks
 #pragma unroll
-            for (int q = 0; q < MS / 2; ++q)
-                reinterpret_cast<double2*>(up)[q] = make_double2(un[2 * q], un[2 * q + 1]);
+                for (int q = 0; q < MS / 2; ++q)
+                    *reinterpret_cast<double2*>(tile + G::at(jl, a + 2 * q)) = make_double2(un[2 * q], un[2 * q + 1]);
+                __syncwarp();
+                double2* gw = reinterpret_cast<double2*>(v.U + pb + static_cast<size_t>(jw) * NY);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int e = q * 64 + 2 * ln;
+                    gw[q * 32 + ln] = *reinterpret_cast<const double2*>(tile + G::at(jw + e / NY, e % NY));
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < MS / 2; ++q)
+                    reinterpret_cast<double2*>(up)[q] = make_double2(un[2 * q], un[2 * q + 1]);
+            }
         }
     }
     for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
