@@ -2168,17 +2168,18 @@ k_plane(BatchView v, int s) {
         // chunks (lane l holds elements 64q + 2l) and are exchanged with the
         // lanes that own them through the warp's tile rows, which are free once
         // every lane has read its x; loads are in flight through the solve
-        constexpr bool early_u = G::MINB == 1;
+        constexpr bool early_u = G::MINB == 1;       // registers for U in flight through the solve
         constexpr int WROWS = 32 / LY;
-        static_assert(!early_u || (WROWS * NY == 512 && ALL_LIVE), "staged U: 512 doubles per warp");
+        constexpr bool stage_u = WROWS * NY == 512 && ALL_LIVE;  // all benchmarked shapes
         const int jw = jl & ~(WROWS - 1);  // the warp's first row
         const int ln = tid & 31;
-        double2 us[early_u ? 8 : 1];
-        if constexpr (early_u) {
+        double2 us[stage_u ? 8 : 1];
+        auto load_us = [&] {
             const double2* gw = reinterpret_cast<const double2*>(v.U + pb + static_cast<size_t>(jw) * NY);
 #pragma unroll
             for (int q = 0; q < 8; ++q) us[q] = gw[q * 32 + ln];
-        }
+        };
+        if constexpr (stage_u && early_u) load_us();
         double x[MS], cs[MS], al[MS];
 #pragma unroll
         for (int q = 0; q < MS / 2; ++q) {
@@ -2279,7 +2280,8 @@ k_plane(BatchView v, int s) {
             }
         }
         if (live) {
-            if constexpr (early_u) {
+            if constexpr (stage_u) {
+                if constexpr (!early_u) load_us();
                 __syncwarp();  // every lane has read its x from the warp's tile rows
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
@@ -2317,7 +2319,7 @@ k_plane(BatchView v, int s) {
                 if (sy == LY - 1 && ymaxD) un[MS - 1] = vtab[6 * NV];
             }
             if (!(v.dbg & 32)) guard_seg<MS>(v, p, s, (static_cast<size_t>(i) * NV + j) * NY + a, un, bound);
-            if constexpr (early_u) {  // back through the tile rows, out as coalesced chunks
+            if constexpr (stage_u) {  // back through the tile rows, out as coalesced chunks
 #pragma unroll
                 for (int q = 0; q < MS / 2; ++q)
                     *reinterpret_cast<double2*>(tile + G::at(jl, a + 2 * q)) = make_double2(un[2 * q], un[2 * q + 1]);
