@@ -1630,16 +1630,6 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         return;
     }
     if (blockIdx.x == 0 && tid == 0) st.maxdelta_bits = 0ull;
-    // the face buffer of step s+1 (read from the next step on), spread over the
-    // grid's threads after the march (replaces a k_faces launch per step)
-    auto next_faces = [&] {
-        if (v.fb_next && s + 1 < v.S) {
-            const int nb = gridDim.x;
-            double* fbn = v.fb_next + static_cast<size_t>(p) * v.fb_stride;
-            for (int e = tid * nb + blockIdx.x; e < v.fb_stride; e += nt * nb)
-                fbn[e] = face_entry(v, p, s + 1, e);
-        }
-    };
     if (jdir) {
         // a Dirichlet v face: every column is an identity line, dU1 = dU0 =
         // face(t_next) - U (solver.cpp:111-116, 127), with the face precedence
@@ -1659,7 +1649,6 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             if (i == nr - 1 && rmaxD) f = rmaxv;
             dcol[static_cast<size_t>(i) * SR] = f - u0;
         }
-        next_faces();
         return;
     }
 
@@ -1882,7 +1871,6 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         if (r < M - 1) b = -cs[r] * b;
         dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(al[r], left, x[r]));
     }
-    next_faces();
 }
 
 inline size_t pa_smem(int nr) {
@@ -2340,6 +2328,34 @@ k_plane(BatchView v, int s) {
     for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
     if ((tid & 31) == 0 && md > 0.0)
         atomicMax(&st.maxdelta_bits, static_cast<unsigned long long>(__double_as_longlong(md)));
+    // this plane's entries of the face table of step s+1 (read from the next step
+    // on; the step's own table was filled one step earlier or by k_faces): the
+    // v faces (i, k) of this CTA's rows, the y faces (i), and on the r-face
+    // planes the r faces (k); one closed form per entry (model.cpp:48-54)
+    if (v.fb_next && s + 1 < v.S) {
+        double* fbn = v.fb_next + static_cast<size_t>(p) * v.fb_stride;
+        const double* stp = step_row(v, p, s + 1);
+        const Tab T = tables(v, p);
+        const bool rface = i == 0 || i == nr - 1;
+        const int n_ent = (c == 0 ? 2 : 0) + 2 * (NY / CS) + (rface && c == 0 ? NY : 0);
+        for (int e = tid; e < n_ent; e += NT) {
+            int face, k = 0, q;
+            if (e < 2 * (NY / CS)) {  // v faces: this CTA's share of k
+                face = e < NY / CS ? F_VMAX : F_VMIN;
+                k = c * (NY / CS) + (e < NY / CS ? e : e - NY / CS);
+                q = 2 * NY + 2 * nr + (face == F_VMAX ? 0 : nr * NY) + i * NY + k;
+            } else if (c == 0 && e < 2 * (NY / CS) + 2) {  // y faces
+                face = e == 2 * (NY / CS) ? F_YMAX : F_YMIN;
+                k = face == F_YMAX ? NY - 1 : 0;
+                q = 2 * NY + (face == F_YMAX ? 0 : nr) + i;
+            } else {  // r faces of the boundary planes
+                face = i == nr - 1 ? F_RMAX : F_RMIN;
+                k = e - 2 * (NY / CS) - 2;
+                q = (face == F_RMAX ? 0 : NY) + k;
+            }
+            fbn[q] = (v.dmask >> face & 1) ? face_value(v.pc[p], stp, T, face, i, k) : 0.0;
+        }
+    }
 }
 
 template <int NV, int NY, int CS, int NT, int MB = 0>
@@ -2430,7 +2446,7 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         const char* e = std::getenv("HJMSV_FOLD");
         return e ? std::atoi(e) : -1;
     }();
-    const bool fold = pa && (fold_env < 0 ? v.P <= 8 : fold_env > 0);
+    const bool fold = plane && fold_env != 0;  // pass B fills the next step's face table
     if (!fold) w.fb_next = nullptr;
     if (!fold || (flags & STEP_FIRST)) {  // otherwise pass A of step s-1 filled it
         k_faces<<<dim3((v.fb_stride + 255) / 256, v.P), 256, 0, stream>>>(v, s);
