@@ -2052,21 +2052,25 @@ k_plane(BatchView v, int s) {
             }
         }
         cluster_sync();
-        if (vwork && tid < NY && !colD) {  // forward carries over all segments
+        // every thread runs the column's forward carry chain over the segment
+        // end values itself and keeps the carry into each of its segments (no
+        // serial pass by one thread per column, no extra barrier)
+        double cins[TPT];
+        if (vs) {
             double cc = 0.0;
 #pragma unroll
             for (int t = 0; t < SV; ++t) {
-                const double endv = car[G::ci(t, kc)];
-                car[G::ci(t, kc)] = cc;
-                cc = fma(vtab[3 * NV + (t * MS + MS - 1)], cc, endv);
+#pragma unroll
+                for (int q = 0; q < TPT; ++q)
+                    if (t == c * SVL + sl0 + q * SSTEP) cins[q] = cc;
+                cc = fma(vtab[3 * NV + (t * MS + MS - 1)], cc, car[G::ci(t, kc)]);
             }
         }
-        __syncthreads();
         if (vs) {
 #pragma unroll
             for (int q = 0; q < TPT; ++q) {
                 const int sv = c * SVL + sl0 + q * SSTEP, ag = sv * MS;
-                const double cin = car[G::ci(sv, kc)];
+                const double cin = cins[q];
                 double xb = 0.0;
 #pragma unroll
                 for (int r = MS - 1; r >= 0; --r) {
@@ -2078,20 +2082,21 @@ k_plane(BatchView v, int s) {
             }
         }
         cluster_sync();
-        if (vwork && tid < NY && !colD) {  // backward carries from the top
+        double cos_[TPT];  // backward carries into this thread's segments, from the top
+        if (vs) {
             double cc = 0.0;
 #pragma unroll
             for (int t = SV - 1; t >= 0; --t) {
-                const double firstv = car[SV * G::CP + G::ci(t, kc)];
-                car[SV * G::CP + G::ci(t, kc)] = cc;
-                cc = fma(vtab[4 * NV + t * MS], cc, firstv);
+#pragma unroll
+                for (int q = 0; q < TPT; ++q)
+                    if (t == c * SVL + sl0 + q * SSTEP) cos_[q] = cc;
+                cc = fma(vtab[4 * NV + t * MS], cc, car[SV * G::CP + G::ci(t, kc)]);
             }
         }
-        __syncthreads();
 #pragma unroll
         for (int q = 0; q < TPT; ++q) {
-            const int a = (sl0 + q * SSTEP) * MS, sv = c * SVL + sl0 + q * SSTEP;
-            const double co = vs ? car[SV * G::CP + G::ci(sv, kc)] : 0.0;
+            const int a = (sl0 + q * SSTEP) * MS;
+            const double co = vs ? cos_[q] : 0.0;
 #pragma unroll
             for (int r = 0; r < MS; ++r) {
                 const double xq = vs ? fma(vtab[4 * NV + j0 + a + r], co, xv[q][r]) : xv[q][r];
