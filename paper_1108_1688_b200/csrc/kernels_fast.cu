@@ -187,7 +187,7 @@ __device__ __forceinline__ bool seg_solve(int m, double (&x)[M], double (&cs)[M]
     // 1/piv_r = P_{r-1}/P_r, so the recurrence chain is one FMA per row and the
     // reciprocal is off it; y' and alpha' then carry one FMA / MUL per row.
     double pm1 = 1.0, pm2 = 0.0, uprev = 0.0, yprev = 0.0, aprev = 0.0;
-    bool ok = true;
+    unsigned badm = 0u;  // rows with |pivot| < 1e-300 (solver.cpp:44-52); the first one is reported
 #pragma unroll
     for (int r = 0; r < M; ++r) {
         if (r < m) {
@@ -195,10 +195,7 @@ __device__ __forceinline__ bool seg_solve(int m, double (&x)[M], double (&cs)[M]
             row(r, l, d, u);
             const double P = r == 0 ? d : fma(d, pm1, -(l * uprev) * pm2);
             const double rp = pm1 * frcp(P);
-            if (fabs(rp) > 1e300 && ok) {  // |pivot| < 1e-300 (solver.cpp:44-52)
-                ok = false;
-                bad_r = r;
-            }
+            badm |= (fabs(rp) > 1e300 ? 1u : 0u) << r;
             const bool last = r == m - 1;
             const double lrp = l * rp;
             const double c = last ? 0.0 : u * rp;  // the last row's upper couples outside
@@ -239,7 +236,8 @@ __device__ __forceinline__ bool seg_solve(int m, double (&x)[M], double (&cs)[M]
     yF = yn;
     aF = an;
     bF = bn;
-    return ok;
+    if (badm) bad_r = __ffs(badm) - 1;
+    return badm == 0u;
 }
 
 // seg_solve with the same arithmetic in a latency-friendlier order, for
