@@ -2008,9 +2008,11 @@ k_plane(BatchView v, int s) {
         if (tid < 2)  // this plane's y-face values at t_next: YMAX, YMIN
             vtab[6 * NV + tid] = __ldg(v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY + tid * nr + i);
         for (int e = tid; e < NY; e += NT) {  // padded so the segments hit distinct banks
+            // scaled by theta dt: a y-row coefficient is one FMA, th g6 = h1 (th S6) + (th T6)
             const int cc = 2 * ((e >> 4) * 17 + (e & 15));
-            ytab[cc] = F.Y[kFY * e + FY_S6];
-            ytab[cc + 1] = F.Y[kFY * e + FY_T6];
+            const double thp = v.pc[p].theta_dt;
+            ytab[cc] = thp * F.Y[kFY * e + FY_S6];
+            ytab[cc + 1] = thp * F.Y[kFY * e + FY_T6];
         }
     }
     __syncthreads();
@@ -2182,14 +2184,11 @@ k_plane(BatchView v, int s) {
         double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
         if (solve && !(v.dbg & 4)) {
             const double h1 = a_i * vtab[5 * NV + j];
-            double lr[MS];
-            double g60 = 0.0;
+            double lr[MS];  // th g6 / (2 dxy) per row
 #pragma unroll
             for (int r = 0; r < MS; ++r) {
                 const double2 st6 = reinterpret_cast<const double2*>(ytab)[sy * 17 + r];
-                const double g6h = fma(h1, st6.x, st6.y);
-                if (r == 0) g60 = g6h;
-                lr[r] = th * g6h;
+                lr[r] = fma(h1, st6.x, st6.y);
             }
             double f0d = dint, f0u = -lr[0];
             if (sy == 0) {  // row 0 (discretization.cpp:274-289), folded (solver.cpp:28-40)
@@ -2197,10 +2196,10 @@ k_plane(BatchView v, int s) {
                 f0u = 0.0;
                 if (!yminD) {
                     if (v.y_order == 1) {
-                        f0d = fma(th, fma(2.0, g60, react), 1.0);
+                        f0d = fma(2.0, lr[0], fma(th, react, 1.0));
                         f0u = -2.0 * lr[0];
                     } else {
-                        f0d = fma(th, fma(3.0, g60, react), 1.0);
+                        f0d = fma(3.0, lr[0], fma(th, react, 1.0));
                         f0u = -4.0 * lr[0];
                         const double s20 = lr[0];
                         const double l1 = lr[1], u1 = -lr[1];
