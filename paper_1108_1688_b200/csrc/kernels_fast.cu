@@ -1511,6 +1511,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <int NV, int NY, bool SCAN>
 __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
+    // launched as a programmatic dependent of the previous kernel: everything
+    // below reads what it wrote (no-op without a programmatic dependency)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     constexpr int M = 16;
     constexpr int SR = NV * NY;
     extern __shared__ double sm[];
@@ -1926,6 +1929,7 @@ struct PlaneGeom {
 template <int NV, int NY, int CS, int NTX, int MB>
 __global__ void __launch_bounds__(NTX, (PlaneGeom<NV, NY, CS, NTX, MB>::MINB))
 k_plane(BatchView v, int s) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of pass A
     using G = PlaneGeom<NV, NY, CS, NTX, MB>;
     constexpr int MS = G::MS, LY = G::LY, SV = G::SV, SVL = G::SVL, RV = G::RV, NT = G::NT;
     extern __shared__ double sm[];
@@ -2360,6 +2364,30 @@ k_plane(BatchView v, int s) {
     }
 }
 
+// programmatic dependent launch of the two passes (HJMSV_PDL=0 turns it off)
+int pdl_enabled() {
+    static const int on = [] {
+        const char* e = std::getenv("HJMSV_PDL");
+        return e ? std::atoi(e) : 1;
+    }();
+    return on;
+}
+
+template <class K>
+void launch_pdl(K kernel, dim3 g, dim3 b, size_t sm, cudaStream_t stream, const BatchView& v, int s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, v, s);
+}
+
 template <int NV, int NY, int CS, int NT, int MB = 0>
 void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
     using G = PlaneGeom<NV, NY, CS, NT, MB>;
@@ -2374,13 +2402,15 @@ void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = G::SMEM;
     cfg.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CS;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // launch ahead, wait in-kernel
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaLaunchKernelEx(&cfg, k_plane<NV, NY, CS, NT, MB>, v, s);
 }
 
@@ -2475,15 +2505,15 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         }();
         (void)attr;
         switch (shape) {
-            case 32: k_pa<32, 32, false><<<g, b, sm, stream>>>(v, s); break;
-            case 64: k_pa<64, 64, false><<<g, b, sm, stream>>>(v, s); break;
+            case 32: launch_pdl(k_pa<32, 32, false>, g, b, sm, stream, v, s); break;
+            case 64: launch_pdl(k_pa<64, 64, false>, g, b, sm, stream, v, s); break;
             case 128:
-                if (scan) k_pa<128, 128, true><<<g, b, sm, stream>>>(v, s);
-                else k_pa<128, 128, false><<<g, b, sm, stream>>>(v, s);
+                if (scan) launch_pdl(k_pa<128, 128, true>, g, b, sm, stream, v, s);
+                else launch_pdl(k_pa<128, 128, false>, g, b, sm, stream, v, s);
                 break;
             default:
-                if (scan) k_pa<256, 256, true><<<g, b, sm, stream>>>(v, s);
-                else k_pa<256, 256, false><<<g, b, sm, stream>>>(v, s);
+                if (scan) launch_pdl(k_pa<256, 256, true>, g, b, sm, stream, v, s);
+                else launch_pdl(k_pa<256, 256, false>, g, b, sm, stream, v, s);
                 break;
         }
         mark(0, "fx_explicit_sweep_r", 16.0);
