@@ -240,84 +240,6 @@ __device__ __forceinline__ bool seg_solve(int m, double (&x)[M], double (&cs)[M]
     return badm == 0u;
 }
 
-// seg_solve with the same arithmetic in a latency-friendlier order, for
-// segments whose rows are cheap to regenerate (row() is called twice per row):
-// (1) the pivot continuants P_r (one FMA per row on the chain), (2) all M
-// reciprocals at once (independent), (3) the y and alpha recurrences (one op
-// per row each), (4) the back-substitution. The per-row schedule of seg_solve
-// puts a reciprocal (MUFU + 4 FP64 ops) between consecutive rows; here the
-// reciprocals overlap. Results are bit-identical to seg_solve.
-template <int M, class RowFn>
-__device__ __forceinline__ bool seg_solve_ilp(double (&x)[M], double (&cs)[M], double (&al)[M],
-                                              double& yF, double& aF, double& bF, double& yL,
-                                              double& aL, double& bL, int& bad_r, RowFn row) {
-    double rp[M];  // P_r, then P_{r-1}/P_r
-    double sc7 = 1.0;
-    {
-        double pm1 = 1.0, pm2 = 0.0, uprev = 0.0;
-#pragma unroll
-        for (int r = 0; r < M; ++r) {
-            double l, d, u;
-            row(r, l, d, u);
-            const double P = r == 0 ? d : fma(d, pm1, -(l * uprev) * pm2);
-            rp[r] = P;
-            uprev = u;
-            pm2 = pm1;
-            pm1 = P;
-            if (r % 8 == 7) {  // exact power-of-two rescaling keeps P in range
-                const int e = ((__double2hiint(pm1) >> 20) & 0x7ff) - 1023;
-                const double sc = __hiloint2double((1023 - e) << 20, 0);
-                pm1 *= sc;
-                pm2 *= sc;
-                if (r == 7) sc7 = sc;
-            }
-        }
-    }
-    static_assert(M <= 16, "one rescale carried between the phases");
-    unsigned badm = 0u;
-#pragma unroll
-    for (int r = M - 1; r >= 0; --r) {  // descending: P_{r-1} is still intact
-        const double pm1 = r == 0 ? 1.0 : (r == 8 ? rp[7] * sc7 : rp[r - 1]);
-        rp[r] = pm1 * frcp(rp[r]);
-        badm |= (fabs(rp[r]) > 1e300 ? 1u : 0u) << r;  // |pivot| < 1e-300 (solver.cpp:44-52)
-    }
-    double yprev = 0.0, aprev = 0.0;
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-        double l, d, u;
-        row(r, l, d, u);
-        const bool last = r == M - 1;
-        const double lrp = l * rp[r];
-        const double c = last ? 0.0 : u * rp[r];
-        const double yy = r == 0 ? x[r] * rp[r] : fma(-lrp, yprev, x[r] * rp[r]);
-        const double aa = r == 0 ? -lrp : -lrp * aprev;
-        if (last) {
-            yL = yy;
-            aL = aa;
-            bL = -u * rp[r];
-        }
-        cs[r] = c;
-        x[r] = yy;
-        al[r] = aa;
-        yprev = yy;
-        aprev = aa;
-    }
-    double yn = yL, an = aL, bn = bL;
-#pragma unroll
-    for (int r = M - 2; r >= 0; --r) {
-        yn = fma(-cs[r], yn, x[r]);
-        an = fma(-cs[r], an, al[r]);
-        bn = -cs[r] * bn;
-        x[r] = yn;
-        al[r] = an;
-    }
-    yF = yn;
-    aF = an;
-    bF = bn;
-    bad_r = badm ? __ffs(badm) - 1 : 0;
-    return badm == 0u;
-}
-
 // The segment solve of seg_solve by a twisted factorisation: rows 0..K-1 are
 // eliminated from the top (LU) and rows M-1..K+1 from the bottom (UL) at the
 // same time, and the two sweeps meet at row K = M/2, so each thread runs two
@@ -543,91 +465,6 @@ __device__ __forceinline__ bool reduced_solve_2way(double* E, int S, int stride,
             e0[7 * fs] = qs;
         }
         qn = qs;
-    }
-    return ok;
-}
-
-// reduced_solve_2way for a compile-time segment count, with the forward
-// recurrence in projective form. With Pp = m/d and Pq = n/d, one pair step is
-//   tA = aL m + yL d,  tB = aL n + bL d,  d' = d - aF tB,
-//   m' = tA + yF tB,   n' = bF tB
-// (den = d'/d, Qc = (aF tA + yF d)/d', Qd = bF d/d', Pp' = m'/d', Pq' = n'/d'),
-// so the loop-carried chain is a multiply and two FMAs; the reciprocal of d'
-// and the stored Qc, Qd, Pp, Pq hang off it. (m, n, d) are rescaled by exact
-// powers of two every four pairs.
-template <int S>
-__device__ __forceinline__ bool reduced_solve_2way_p(double* E, int stride, int fs, bool back,
-                                                     unsigned mask, int partner, int& bad_t) {
-    constexpr int np = S - 1;
-    constexpr int mF = (np + 1) >> 1, mB = np - mF;
-    const int fy0 = back ? 0 : 3, fa0 = back ? 2 : 4, fb0 = back ? 1 : 5;  // end row of s0
-    const int fy1 = back ? 3 : 0, fa1 = back ? 5 : 1, fb1 = back ? 4 : 2;  // first row of s1
-    const int sp = back ? 0 : 3, sq = back ? 2 : 4;                        // scratch Pp, Pq
-    const int n = back ? mB : mF;
-    double m = 0.0, nq = 0.0, d = 1.0, rd = 1.0, Pp = 0.0, Pq = 0.0;
-    bool ok = true;
-#pragma unroll
-    for (int k = 0; k < mF; ++k) {
-        if (k < n) {
-            double* e0 = E + (back ? S - 1 - k : k) * stride;
-            const double* e1 = E + (back ? S - 2 - k : k + 1) * stride;
-            const double aL = e0[fa0 * fs], yL = e0[fy0 * fs], bL = e0[fb0 * fs];
-            const double aF = e1[fa1 * fs], yF = e1[fy1 * fs], bF = e1[fb1 * fs];
-            const double tA = fma(aL, m, yL * d);
-            const double tB = fma(aL, nq, bL * d);
-            const double dn = fma(-aF, tB, d);
-            const double mn = fma(yF, tB, tA);
-            const double nn = bF * tB;
-            const double r = frcp(dn);
-            if (fabs(dn * rd) < 1e-300 && ok) {  // den = 1 - aF B
-                ok = false;
-                bad_t = back ? S - 2 - k : k + 1;
-            }
-            Pp = mn * r;
-            Pq = nn * r;
-            e0[6 * fs] = fma(aF, tA, yF * d) * r;  // Qc
-            e0[7 * fs] = (bF * d) * r;             // Qd
-            e0[sp * fs] = Pp;
-            e0[sq * fs] = Pq;
-            m = mn;
-            nq = nn;
-            d = dn;
-            rd = r;
-            if (k % 4 == 3) {
-                const int ex = ((__double2hiint(d) >> 20) & 0x7ff) - 1023;
-                const double sc = __hiloint2double((1023 - ex) << 20, 0);
-                const double isc = __hiloint2double((1023 + ex) << 20, 0);
-                m *= sc;
-                nq *= sc;
-                d *= sc;
-                rd *= isc;
-            }
-        }
-    }
-    // meet: p_{mF-1} = PpF + PqF q_mF (forward), q_mF = PpB + PqB p_{mF-1} (backward)
-    const double oPp = __shfl_xor_sync(mask, Pp, partner);
-    const double oPq = __shfl_xor_sync(mask, Pq, partner);
-    const double PpF = back ? oPp : Pp, PqF = back ? oPq : Pq;
-    const double PpB = back ? Pp : oPp, PqB = back ? Pq : oPq;
-    const double pm = (PpF + PqF * PpB) / (1.0 - PqF * PqB);
-    const double qm = fma(PqB, pm, PpB);
-    double qn = back ? pm : qm;
-#pragma unroll
-    for (int k = mF - 1; k >= 0; --k) {
-        if (k < n) {
-            double* e0 = E + (back ? S - 1 - k : k) * stride;
-            const double qs = fma(e0[7 * fs], qn, e0[6 * fs]);
-            const double ps = fma(e0[sq * fs], qn, e0[sp * fs]);
-            if (back) {  // reversed pair k is original pair t = S-2-k: p_t = qs, q_t = ps
-                double* et = E + (S - 2 - k) * stride;
-                et[6 * fs] = qs;
-                et[7 * fs] = ps;
-            } else {
-                e0[6 * fs] = ps;
-                e0[7 * fs] = qs;
-            }
-            qn = qs;
-        }
     }
     return ok;
 }
@@ -1478,16 +1315,8 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
 // so dU1 = dU0 there.
 constexpr int kRing = 3;
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-}
 __device__ __forceinline__ void cp_async8s(unsigned dst, const double* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
 }
 // one-shot bulk (TMA engine) copies of contiguous tables into shared memory,
 // completion tracked by an mbarrier (phase 0)
