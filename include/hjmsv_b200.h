@@ -250,15 +250,25 @@ int32_t hjmsv_solver_last_device_ms(hjmsv_solver* h, double* ms);
 /* Number of kernel launches issued by the last step_async call. */
 int32_t hjmsv_solver_last_launches(hjmsv_solver* h, int64_t* launches);
 
-/* Live per-kernel profile: runs `steps` steps with a CUDA event after every
- * launch; returns each kernel's average duration (ms), its ALGORITHMIC bytes
- * per launch (bytes/point x points; SURVEY §8d accounting), the launch count,
- * and names (name_len bytes each). Used by bench.py for the roofline. */
+/* Live per-kernel profile (FAST mode): runs `steps` steps launched exactly as
+ * a handle's first march (direct launches, programmatic dependent launch),
+ * every block recording its start/end on the device clock; returns each
+ * kernel slot's average duration (ms, span of its blocks per launch), its
+ * ALGORITHMIC bytes per launch (bytes/point x points; SURVEY §8d accounting),
+ * the launch count, the names (name_len bytes each) and the event-timed
+ * duration of the whole profiled sequence (march_ms, may be null). Used by
+ * bench.py for the roofline. */
+int32_t hjmsv_solver_kernel_timeline(hjmsv_solver* h, int32_t steps, int32_t max_kernels,
+                                     double* avg_ms, double* alg_bytes, int64_t* launches,
+                                     int32_t* n_kernels, char* names, int32_t name_len,
+                                     double* march_ms);
+/* hjmsv_solver_kernel_timeline without march_ms. */
 int32_t hjmsv_solver_kernel_profile(hjmsv_solver* h, int32_t steps, int32_t max_kernels,
                                     double* avg_ms, double* alg_bytes, int64_t* launches,
                                     int32_t* n_kernels, char* names, int32_t name_len);
 
-/* ---- stage entry points (parity tests: the reference's stage oracles) ---- */
+/* ---- stage entry points (parity tests: the reference's stage oracles) ----
+ * They run on the calling thread's current CUDA device (cudaSetDevice). */
 /* SpatialOperator::apply_operator after coefficients().prepare(t) (discretization.cpp:302-364) */
 int32_t hjmsv_apply_operator(const hjmsv_problem* p, const hjmsv_solver_config* cfg, double t,
                              const double* u, double* out, int32_t mode);
@@ -267,7 +277,11 @@ int32_t hjmsv_douglas_step(const hjmsv_problem* p, const hjmsv_solver_config* cf
                            const double* u_in, double t_from, double dt, double* u_out,
                            double* max_delta, int32_t mode);
 /* Batched thomas_solve_inplace (solver.cpp:22-57) of `count` lines of length n
- * (arrays are count*n, line-major); super2 is per line. Runs on device 0. */
+ * (arrays are count*n, line-major); super2 is per line. mode HJMSV_MODE_STRICT:
+ * the reference's sequential Thomas; HJMSV_MODE_FAST: the partition method of
+ * pass A's r-lines (16-row segments, lane-scan reduced system, n <= 512);
+ * HJMSV_THOMAS_FAST_TWISTED: the same with pass B's twisted segment solve. */
+#define HJMSV_THOMAS_FAST_TWISTED 2
 int32_t hjmsv_thomas_batch(int32_t n, int32_t count, const double* lower, const double* diag,
                            const double* upper, const double* super2, double* rhs,
                            int32_t mode);

@@ -61,6 +61,12 @@ class Checker:
             fn = getattr(self.lib, prefix + name)
             fn.restype, fn.argtypes = res, args
         if prefix == "ref_":
+            self.lib.ref_session_create.restype = ctypes.c_void_p
+            self.lib.ref_session_create.argtypes = [P, C]
+            self.lib.ref_session_steps.restype = c_int
+            self.lib.ref_session_steps.argtypes = [ctypes.c_void_p, c_int, PD]
+            self.lib.ref_session_destroy.restype = None
+            self.lib.ref_session_destroy.argtypes = [ctypes.c_void_p]
             self.lib.ref_mix_seed.restype = c_uint64
             self.lib.ref_mix_seed.argtypes = [c_uint64, c_uint64]
             self.lib.ref_mc_price.restype = c_int
@@ -88,6 +94,10 @@ class Checker:
         if raise_on_error:
             self._chk(code)
         return g.reshape(p.shape), rep.as_dict(), code, (self.error() if code else "")
+
+    def session(self, p: ProblemSpec, cfg: Optional[SolverConfig] = None) -> "RefSession":
+        """Resumable reference march (setup once, then timed douglas_step loops)."""
+        return RefSession(self, p, cfg)
 
     def initial_level(self, p: ProblemSpec, cfg: Optional[SolverConfig] = None):
         cp, cc = p.to_c(), (cfg or SolverConfig()).to_c()
@@ -183,6 +193,33 @@ class Checker:
         reps = (A.CReport * len(problems))()
         code = self._f("batch_run")(arr, len(problems), ctypes.byref(cc), threads, _ptr(prices), reps)
         return prices, [r.as_dict() for r in reps], code
+
+
+class RefSession:
+    """ref_session_*: run()'s setup once, then `steps(n)` advances the march with
+    the reference's douglas_step and returns the stepping loop's own seconds."""
+
+    def __init__(self, chk: Checker, p: ProblemSpec, cfg: Optional[SolverConfig] = None):
+        self.chk = chk
+        self._keep = (p.to_c(), (cfg or SolverConfig()).to_c())
+        self.h = chk.lib.ref_session_create(ctypes.byref(self._keep[0]), ctypes.byref(self._keep[1]))
+        if not self.h:
+            raise RuntimeError(chk.error())
+
+    def steps(self, n: int) -> float:
+        secs = c_double()
+        code = self.chk.lib.ref_session_steps(self.h, n, ctypes.byref(secs))
+        if code:
+            raise RuntimeError(f"[{A.STATUS_NAMES[code]}] {self.chk.error()}")
+        return secs.value
+
+    def close(self):
+        if self.h:
+            self.chk.lib.ref_session_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 _cache = {}

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -322,6 +323,72 @@ int ref_run(const hjmsv_problem* p, const hjmsv_solver_config* c, int steps_to_d
     if (rep) *rep = r;
     return code;
 }
+
+// A resumable march for the CPU baseline legs of bench.py: create() does the
+// setup of run() (terminal fill + smooth_terminal, coefficient field, operator;
+// solver.cpp:219-236) once, steps() advances the same march with douglas_step
+// (solver.cpp:240-251, indexed time levels when the problem asks for them) and
+// returns the time of the stepping loop alone, as SURVEY §8d's timed region.
+struct RefSession {
+    PdeProblem pb;
+    SolverConfig cfg;
+    std::unique_ptr<Grid3> grid;
+    std::unique_ptr<HjmCoefficientField> coeffs;
+    std::unique_ptr<SpatialOperator> op;
+    int n_steps = 0, step = 0;
+    bool indexed = false;
+    double dt = 0.0;
+};
+
+void* ref_session_create(const hjmsv_problem* p, const hjmsv_solver_config* c) {
+    RefSession* out = nullptr;
+    const int code = guarded([&] {
+        auto ses = std::make_unique<RefSession>();
+        ses->cfg = to_config(c);
+        ses->cfg.validate();
+        ses->pb = to_problem(*p);
+        ses->grid = std::make_unique<Grid3>(initial_level(ses->pb, ses->cfg, *p));
+        Grid3& g = *ses->grid;
+        ses->coeffs = std::make_unique<HjmCoefficientField>(g.r, g.v, g.y, ses->pb.model, ses->pb.curve,
+                                                            ses->pb.r0);
+        ses->op = std::make_unique<SpatialOperator>(
+            g.r, g.v, g.y, *ses->coeffs, ses->pb.boundary,
+            SpatialOperator::Options{ses->cfg.y_boundary_order, ses->cfg.r_boundary_order});
+        ses->n_steps = resolve_steps(*p, ses->cfg);
+        ses->dt = ses->pb.maturity / ses->n_steps;
+        ses->indexed = p->time_levels == HJMSV_TIME_INDEXED;
+        out = ses.release();
+    });
+    (void)code;
+    return out;
+}
+
+// advances `count` steps (restarting from the terminal level is the caller's
+// business: past the last step it wraps to step 0 of a fresh time sequence on
+// the current level, which keeps the per-step work identical)
+int ref_session_steps(void* h, int count, double* loop_seconds) {
+    auto* ses = static_cast<RefSession*>(h);
+    double secs = 0.0;
+    const int code = guarded([&] {
+        if (!ses) throw std::invalid_argument("null session");
+        Grid3& g = *ses->grid;
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int q = 0; q < count; ++q) {
+            if (ses->step >= ses->n_steps) {
+                ses->step = 0;
+                g.time = ses->pb.maturity;
+            }
+            if (ses->indexed) g.time = ses->pb.maturity - ses->step * ses->dt;
+            douglas_step(g, *ses->op, ses->dt, ses->cfg);
+            ++ses->step;
+        }
+        secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+    if (loop_seconds) *loop_seconds = secs;
+    return code;
+}
+
+void ref_session_destroy(void* h) { delete static_cast<RefSession*>(h); }
 
 // douglas_step on an injected level (solver.hpp:45-47)
 int ref_douglas_step(const hjmsv_problem* p, const hjmsv_solver_config* c, const double* u_in,

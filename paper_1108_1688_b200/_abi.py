@@ -111,6 +111,8 @@ SIGNATURES = {
     "hjmsv_solver_last_launches": (I32, [HP, POINTER(c_int64)]),
     "hjmsv_solver_kernel_profile": (I32, [HP, I32, I32, PD, PD, POINTER(c_int64), POINTER(I32),
                                           ctypes.c_char_p, I32]),
+    "hjmsv_solver_kernel_timeline": (I32, [HP, I32, I32, PD, PD, POINTER(c_int64), POINTER(I32),
+                                           ctypes.c_char_p, I32, PD]),
     "hjmsv_apply_operator": (I32, [POINTER(CProblem), POINTER(CSolverConfig), c_double, PD, PD, I32]),
     "hjmsv_douglas_step": (I32, [POINTER(CProblem), POINTER(CSolverConfig), PD, c_double, c_double, PD, PD, I32]),
     "hjmsv_thomas_batch": (I32, [I32, I32, PD, PD, PD, PD, PD, I32]),

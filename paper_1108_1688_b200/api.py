@@ -191,20 +191,26 @@ class Solver:
         _check(self.lib.hjmsv_solver_last_device_ms(self.h, ctypes.byref(ms)))
         return ms.value
 
-    def kernel_profile(self, steps: int):
-        """Per-kernel average ms and algorithmic bytes per launch over `steps` steps."""
+    def kernel_profile(self, steps: int, with_total: bool = False):
+        """Per-kernel average ms (device timeline, launched as a first march) and
+        algorithmic bytes per launch over `steps` steps; with_total also returns
+        the event-timed ms of the whole profiled sequence."""
         K, L = 16, 64
         ms, by = np.zeros(K), np.zeros(K)
         n, nk = ctypes.c_int64(), ctypes.c_int32()
+        total = ctypes.c_double()
         names = ctypes.create_string_buffer(K * L)
-        _check(self.lib.hjmsv_solver_kernel_profile(self.h, steps, K, _ptr(ms), _ptr(by),
-                                                    ctypes.byref(n), ctypes.byref(nk), names, L))
+        _check(self.lib.hjmsv_solver_kernel_timeline(self.h, steps, K, _ptr(ms), _ptr(by),
+                                                     ctypes.byref(n), ctypes.byref(nk), names, L,
+                                                     ctypes.byref(total)))
         out = []
         for q in range(nk.value):
             nm = names.raw[q * L:(q + 1) * L].split(b"\0", 1)[0].decode()
             if not nm:  # index slot unused by this step variant
                 continue
             out.append({"name": nm, "avg_ms": float(ms[q]), "alg_bytes": float(by[q])})
+        if with_total:
+            return out, n.value, total.value
         return out, n.value
 
     def last_launches(self) -> int:
@@ -255,7 +261,12 @@ def douglas_step(problem: ProblemSpec, u: np.ndarray, t_from: float, dt: float,
 
 
 def thomas_batch(lower, diag, upper, super2, rhs, mode="strict") -> np.ndarray:
+    """Batched thomas_solve_inplace (solver.cpp:22-57). mode "strict": the
+    reference's Thomas; "fast": pass A's partition solver; "fast_twisted": pass
+    B's twisted segment solver (both n <= 512)."""
     lib = A.load()
+    if mode == "fast_twisted":
+        mode = 2
     lower, diag, upper, rhs = (np.ascontiguousarray(x, dtype=np.float64) for x in (lower, diag, upper, rhs))
     count, n = rhs.shape
     s2 = np.ascontiguousarray(super2, dtype=np.float64).reshape(count)

@@ -70,6 +70,14 @@ int32_t guarded(F&& f) {
     }
 }
 
+// Stage entry points (apply_operator, douglas_step, thomas_batch) run on the
+// calling thread's current device, the CUDA runtime convention.
+int current_device() {
+    int d = 0;
+    cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+    return d;
+}
+
 // Device buffers come from the current device's stream-ordered memory pool with
 // an unbounded release threshold: a handle's arrays go back to the pool on
 // destroy and are reused by the next handle without returning memory to the
@@ -274,7 +282,9 @@ std::string status_message(hjmsv_solver* h, int p, const DevStatus& ds, int* cod
         h->stage ? std::string()
                  : "step " + std::to_string(ds.fail_step) + "/" + std::to_string(h->S) + ": ";
     *row = -1;
-    if (ds.fail_code == HJMSV_SINGULAR_PIVOT) {
+    // a singular pivot of the failing step wins over a guard hit of the same
+    // step: the reference's sweeps all run before guard_finite (solver.cpp:121-176)
+    if (ds.pivot_key != ~0ull) {
         *code = HJMSV_SINGULAR_PIVOT;
         *row = static_cast<int>(ds.pivot_key & 0xFFFFFull);
         return prefix + "thomas_solve: singular pivot at row " + std::to_string(*row);
@@ -545,92 +555,107 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
 }
 
 struct ProfCtx {
-    cudaStream_t stream;
-    std::vector<cudaEvent_t>* events;
-    std::vector<std::string>* names;
+    std::vector<std::string>* names;  // by kernel slot
     std::vector<double>* bytes;
-    std::vector<int>* idx;
 };
 
 void prof_after(void* vctx, int idx, const char* name, double b) {
     auto* c = static_cast<ProfCtx*>(vctx);
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, c->stream);
-    c->events->push_back(e);
-    c->names->push_back(name);
-    c->bytes->push_back(b);
-    c->idx->push_back(idx);
+    if (idx >= static_cast<int>(c->names->size())) {
+        c->names->resize(idx + 1);
+        c->bytes->resize(idx + 1, 0.0);
+    }
+    (*c->names)[idx] = name;
+    (*c->bytes)[idx] = b;
 }
 
 }  // namespace
 
 extern "C" {
 
-int32_t hjmsv_solver_kernel_profile(hjmsv_solver* h, int32_t steps, int32_t max_kernels,
-                                    double* avg_ms, double* alg_bytes, int64_t* launches_out,
-                                    int32_t* n_kernels, char* names, int32_t name_len) {
+// Per-kernel durations inside a march launched exactly as the first march of a
+// handle (direct launches, programmatic dependent launch between the passes):
+// every block of every FAST kernel records its start (after the programmatic
+// wait) and end on %globaltimer into a per-(step, kernel) min/max pair, so a
+// kernel's duration is the span of its own blocks and the durations of one
+// step add up to at most the step (no host events between the launches).
+int32_t hjmsv_solver_kernel_timeline(hjmsv_solver* h, int32_t steps, int32_t max_kernels,
+                                     double* avg_ms, double* alg_bytes, int64_t* launches_out,
+                                     int32_t* n_kernels, char* names, int32_t name_len,
+                                     double* march_ms) {
     return guarded([&] {
         if (!h || !avg_ms || !alg_bytes || !n_kernels) throw std::invalid_argument("null argument");
+        if (h->mode != HJMSV_MODE_FAST) throw Failure(HJMSV_UNSUPPORTED, "kernel timeline: FAST mode only");
         CK(cudaSetDevice(h->device));
         const int count = std::min(steps, h->S - h->step);
-        std::vector<cudaEvent_t> ev;
+        if (count < 1) throw std::invalid_argument("no steps left to profile (reset first)");
         std::vector<std::string> nm;
         std::vector<double> by;
-        std::vector<int> ix;
-        ProfCtx ctx{h->stream, &ev, &nm, &by, &ix};
+        ProfCtx ctx{&nm, &by};
         LaunchHook hook;
         hook.after = prof_after;
         hook.ctx = &ctx;
-        cudaEvent_t start;
-        CK(cudaEventCreate(&start));
-        CK(cudaEventRecord(start, h->stream));
+        const size_t n_tl = static_cast<size_t>(count) * kTlSlots;
+        std::vector<unsigned long long> tl(2 * n_tl);
+        for (size_t q = 0; q < n_tl; ++q) {
+            tl[2 * q] = ~0ull;
+            tl[2 * q + 1] = 0ull;
+        }
+        unsigned long long* dtl = nullptr;
+        CK(cudaMalloc(&dtl, sizeof(unsigned long long) * tl.size()));
+        CK(cudaMemcpy(dtl, tl.data(), sizeof(unsigned long long) * tl.size(), cudaMemcpyHostToDevice));
+        BatchView v = h->view;
+        // step s of the march writes entry s - h->step
+        v.tl = dtl - 2 * static_cast<size_t>(h->step) * kTlSlots;
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, h->stream));
         long long n = 0;
         for (int s = h->step; s < h->step + count; ++s) {
             const int flags = (s == h->step ? STEP_FIRST : 0) | (s == h->step + count - 1 ? STEP_LAST : 0);
-            if (h->mode == HJMSV_MODE_FAST)
-                fast_step(h->view, s, h->stream, &n, &hook, flags);
-            else
-                strict_step(h->view, s, h->stream, &n, &hook);
+            fast_step(v, s, h->stream, &n, &hook, flags);
         }
+        CK(cudaEventRecord(e1, h->stream));
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(h->stream));
+        float total = 0.f;
+        CK(cudaEventElapsedTime(&total, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        CK(cudaMemcpy(tl.data(), dtl, sizeof(unsigned long long) * tl.size(), cudaMemcpyDeviceToHost));
+        cudaFree(dtl);
         h->step += count;
-        std::vector<double> total;
-        std::vector<int> calls;
-        std::vector<std::string> kn;
-        std::vector<double> kb;
-        cudaEvent_t prev = start;
-        for (size_t q = 0; q < ev.size(); ++q) {
-            float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, prev, ev[q]));
-            prev = ev[q];
-            const int id = ix[q];
-            if (id >= static_cast<int>(total.size())) {
-                total.resize(id + 1, 0.0);
-                calls.resize(id + 1, 0);
-                kn.resize(id + 1);
-                kb.resize(id + 1, 0.0);
-            }
-            total[id] += ms;
-            calls[id] += 1;
-            kn[id] = nm[q];
-            kb[id] = by[q] * static_cast<double>(h->N) * h->P;
-        }
-        for (auto e : ev) cudaEventDestroy(e);
-        cudaEventDestroy(start);
-        const int K = std::min<int>(max_kernels, static_cast<int>(total.size()));
+        const int K = std::min<int>(max_kernels, static_cast<int>(std::min<size_t>(nm.size(), kTlSlots)));
         for (int q = 0; q < K; ++q) {
-            avg_ms[q] = calls[q] ? total[q] / calls[q] : 0.0;
-            alg_bytes[q] = kb[q];
+            double sum_ns = 0.0;
+            int calls = 0;
+            for (int s = 0; s < count; ++s) {
+                const unsigned long long a = tl[2 * (static_cast<size_t>(s) * kTlSlots + q)];
+                const unsigned long long b = tl[2 * (static_cast<size_t>(s) * kTlSlots + q) + 1];
+                if (a != ~0ull && b > a) {
+                    sum_ns += static_cast<double>(b - a);
+                    ++calls;
+                }
+            }
+            avg_ms[q] = calls ? 1e-6 * sum_ns / calls : 0.0;
+            alg_bytes[q] = by[q] * static_cast<double>(h->N) * h->P;
             if (names && name_len > 0) {
-                std::strncpy(names + static_cast<size_t>(q) * name_len, kn[q].c_str(), name_len - 1);
+                std::strncpy(names + static_cast<size_t>(q) * name_len, nm[q].c_str(), name_len - 1);
                 names[static_cast<size_t>(q) * name_len + name_len - 1] = 0;
             }
         }
         *n_kernels = K;
         if (launches_out) *launches_out = n;
+        if (march_ms) *march_ms = total;
     });
+}
+
+int32_t hjmsv_solver_kernel_profile(hjmsv_solver* h, int32_t steps, int32_t max_kernels,
+                                    double* avg_ms, double* alg_bytes, int64_t* launches_out,
+                                    int32_t* n_kernels, char* names, int32_t name_len) {
+    return hjmsv_solver_kernel_timeline(h, steps, max_kernels, avg_ms, alg_bytes, launches_out,
+                                        n_kernels, names, name_len, nullptr);
 }
 
 void hjmsv_default_solver_config(hjmsv_solver_config* cfg) {
@@ -1042,7 +1067,7 @@ int32_t hjmsv_apply_operator(const hjmsv_problem* p, const hjmsv_solver_config* 
         ov.faces = false;
         ov.apply_only = true;
         const hjmsv_solver_config c = cfg ? *cfg : default_config();
-        std::unique_ptr<hjmsv_solver> h(create_handle(&q, 1, c, 0, mode, &ov));
+        std::unique_ptr<hjmsv_solver> h(create_handle(&q, 1, c, current_device(), mode, &ov));
         if (mode == HJMSV_MODE_FAST)
             fast_explicit(h->view, 0, h->stream);
         else
@@ -1067,7 +1092,7 @@ int32_t hjmsv_douglas_step(const hjmsv_problem* p, const hjmsv_solver_config* cf
         ov.dt = dt;
         ov.dt_mult = dt;
         const hjmsv_solver_config c = cfg ? *cfg : default_config();
-        std::unique_ptr<hjmsv_solver> h(create_handle(&q, 1, c, 0, mode, &ov));
+        std::unique_ptr<hjmsv_solver> h(create_handle(&q, 1, c, current_device(), mode, &ov));
         status = hjmsv_solver_step(h.get(), 1);
         CK(cudaMemcpyAsync(u_out, h->U, sizeof(double) * h->N, cudaMemcpyDeviceToHost,
                            h->stream));
@@ -1085,7 +1110,11 @@ int32_t hjmsv_thomas_batch(int32_t n, int32_t count, const double* lower, const 
         if (n < 0 || count < 0) throw std::invalid_argument("negative size");
         if (n == 0 || count == 0) return;
         if (!lower || !diag || !upper || !super2 || !rhs) throw std::invalid_argument("null argument");
-        CK(cudaSetDevice(0));
+        if (mode < HJMSV_MODE_STRICT || mode > HJMSV_THOMAS_FAST_TWISTED)
+            throw std::invalid_argument("unknown arithmetic mode");
+        if (mode != HJMSV_MODE_STRICT && n > 512)
+            throw Failure(HJMSV_UNSUPPORTED, "FAST lines hold at most 32 segments of 16 rows (n <= 512)");
+        // the calling thread's current device (cudaSetDevice), as every stage entry point
         const size_t m = static_cast<size_t>(n) * count;
         double *dl = dalloc<double>(m), *dd = dalloc<double>(m), *du = dalloc<double>(m);
         double *ds2 = dalloc<double>(count), *dr = dalloc<double>(m), *dsc = dalloc<double>(m);
@@ -1134,6 +1163,15 @@ int32_t hjmsv_batch_run(const hjmsv_problem* problems, int32_t count,
         const hjmsv_solver_config c = cfg ? *cfg : default_config();
         // contiguous shards of ceil(count/G) problems
         const int per = (count + G - 1) / G;
+        // grids_out holds the problems' grids back to back in input order; each
+        // problem's offset is the prefix sum of nr*nv*ny (dims may differ between shards)
+        std::vector<size_t> goff(static_cast<size_t>(count) + 1, 0);
+        for (int q = 0; q < count; ++q) {
+            const hjmsv_problem& pq = problems[q];
+            if (pq.r.n < 1 || pq.v.n < 1 || pq.y.n < 1)
+                throw std::invalid_argument("axis sizes must be positive");
+            goff[q + 1] = goff[q] + static_cast<size_t>(pq.r.n) * pq.v.n * pq.y.n;
+        }
         std::vector<std::thread> pool;
         std::vector<int> codes(G, HJMSV_OK);
         std::vector<std::string> errs(G);
@@ -1147,18 +1185,20 @@ int32_t hjmsv_batch_run(const hjmsv_problem* problems, int32_t count,
                 if (h) {
                     const int run_code = code;
                     std::vector<double> pr(hi - lo);
-                    code = hjmsv_solver_spot_prices(h, pr.data());
+                    // readout failures are reported too, after the march's own status
+                    int read_code = hjmsv_solver_spot_prices(h, pr.data());
+                    auto keep = [&](int c2) {
+                        if (read_code == HJMSV_OK) read_code = c2;
+                    };
                     for (int q = lo; q < hi; ++q) {
                         hjmsv_report r{};
-                        hjmsv_solver_report(h, q - lo, &r);
+                        keep(hjmsv_solver_report(h, q - lo, &r));
                         if (prices_out)
                             prices_out[q] = r.status == HJMSV_OK ? pr[q - lo] : std::nan("");
                         if (reports_out) reports_out[q] = r;
-                        if (grids_out)
-                            hjmsv_solver_get_grid(h, q - lo,
-                                                  grids_out + static_cast<size_t>(q) * h->N);
+                        if (grids_out) keep(hjmsv_solver_get_grid(h, q - lo, grids_out + goff[q]));
                     }
-                    if (run_code != HJMSV_OK) code = run_code;
+                    code = run_code != HJMSV_OK ? run_code : read_code;
                     hjmsv_solver_destroy(h);
                 }
                 codes[g] = code;

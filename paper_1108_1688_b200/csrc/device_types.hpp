@@ -72,7 +72,12 @@ struct BatchView {
     double* fb_next;      // [P][fb_stride] the next step's values (filled by the last kernel of a step)
     int want_md;          // track max|dU| this step (the last step of a launched sequence)
     int dbg;              // diagnostic switches (HJMSV_DBG; 0 in production)
+    // kernel timeline (profiling runs only, else null): per (step, kernel slot)
+    // the earliest block start and the latest block end in %globaltimer ns, so
+    // per-kernel durations are taken in the launch mode of the timed march
+    unsigned long long* tl;
 };
+constexpr int kTlSlots = 5;  // 0 pass A / explicit, 1 r-lines, 2 pass B / v-lines, 3 y-lines, 4 faces
 
 // fast_step flags: the first step of a launched sequence fills its own face
 // buffer; the last one records max|dU| for the report (solver.cpp:163-167).
@@ -158,6 +163,10 @@ void device_terminal(const BatchView& v, const TermParam* tp, const int* host_ki
 // trilinear readout: out[p] = sum_q w[p*8+q] * U[p][idx[p*8+q]] (instruments.cpp:71-88)
 void gather_spot(const BatchView& v, const long long* idx, const double* w, double* out,
                  cudaStream_t stream);
+// FAST partition-method lines (n <= 512): pass A's r-line solver, or with
+// twisted pass B's y-line solver (kernels_fast.cu k_thomas_fast)
+void fast_thomas_batch(int n, int count, const double* lower, const double* diag, const double* upper,
+                       const double* super2, double* rhs, int* fail_row, bool twisted, cudaStream_t stream);
 // standalone batched Thomas (parity stage test of solver.cpp:22-57)
 void thomas_batch(int n, int count, const double* lower, const double* diag, const double* upper,
                   const double* super2, double* rhs, double* scratch, int* fail_row, int fast,

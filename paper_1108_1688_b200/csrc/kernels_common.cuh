@@ -91,6 +91,40 @@ __device__ __forceinline__ const double* step_row(const BatchView& v, int p, int
     return v.steps + (static_cast<size_t>(p) * v.S + s) * kStepStride;
 }
 
+// A problem stops at a failure recorded in an EARLIER step (the reference threw
+// out of that douglas_step, solver.cpp:241-247). A failure recorded during the
+// current step s (0-based; fail_step = s + 1) does not stop the other blocks of
+// the step, so every singular pivot and guard hit of that step is recorded and
+// the host picks the one the reference reports first (pivots before the guard,
+// lowest index first; capi.cpp status_message). Values <= s were written by
+// earlier launches, so all blocks of one launch (and of one cluster) agree.
+__device__ __forceinline__ bool failed_before(const DevStatus& st, int s) {
+    const int f = st.fail_step;
+    return f != 0 && f <= s;
+}
+
+// kernel timeline (BatchView::tl): block start after the programmatic wait,
+// block end after the block's last store (tl_end syncs the block, so every
+// thread of the block must reach it; tl_end_thread records thread 0 only)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ bool tl_lead() { return threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0; }
+__device__ __forceinline__ void tl_begin(const BatchView& v, int s, int slot) {
+    if (v.tl && tl_lead()) atomicMin(v.tl + 2 * (static_cast<size_t>(s) * kTlSlots + slot), gtimer());
+}
+__device__ __forceinline__ void tl_end(const BatchView& v, int s, int slot) {
+    if (v.tl) {
+        __syncthreads();
+        if (tl_lead()) atomicMax(v.tl + 2 * (static_cast<size_t>(s) * kTlSlots + slot) + 1, gtimer());
+    }
+}
+__device__ __forceinline__ void tl_end_thread(const BatchView& v, int s, int slot) {
+    if (v.tl && tl_lead()) atomicMax(v.tl + 2 * (static_cast<size_t>(s) * kTlSlots + slot) + 1, gtimer());
+}
+
 __device__ __forceinline__ void mark_fail(DevStatus& st, int step1, int code) {
     if (atomicCAS(&st.fail_step, 0, step1) == 0) st.fail_code = code;
 }

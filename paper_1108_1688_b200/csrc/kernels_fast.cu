@@ -29,6 +29,9 @@
 // Parity with the reference is 1e-10 normwise (tests/test_gpu_parity.py).
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <type_traits>
 
 #include <cooperative_groups.h>
@@ -91,9 +94,10 @@ __device__ __forceinline__ bool dir(const BatchView& v, int f) { return v.dmask 
 // nodes (apply_operator, discretization.cpp:302-364), face(t_next) - U on
 // Dirichlet nodes (solver.cpp:111-116). apply_only (stage) writes F(U) and 0.
 __global__ void __launch_bounds__(256) k_fx_explicit(BatchView v, int s) {
+    tl_begin(v, s, 0);
     const int p = blockIdx.z, i = blockIdx.y;
     DevStatus& st = v.st[p];
-    if (st.fail_step) return;
+    if (failed_before(st, s)) return;
     if (blockIdx.x == 0 && i == 0 && threadIdx.x == 0 && threadIdx.y == 0) st.maxdelta_bits = 0ull;
     const int nr = v.nr, nv = v.nv, ny = v.ny;
     const int tk = (ny + 31) >> 5;
@@ -173,6 +177,7 @@ __global__ void __launch_bounds__(256) k_fx_explicit(BatchView v, int s) {
         }
     }
     v.D[off + q] = out;
+    tl_end_thread(v, s, 0);
 }
 
 // ============================================================ partition solve
@@ -562,14 +567,91 @@ __device__ __forceinline__ int reduced_scan(double yF, double aF, double bF, dou
     return bad;
 }
 
+// ============================================================ batched lines (stage test)
+// Lines solved by the FAST partition method exactly as pass A's r-lines (and,
+// with TW, pass B's y-lines) solve theirs: one warp per line, lane t owns rows
+// 16t..16t+15 (rows past n are identity rows), the super2 fold of
+// thomas_solve_inplace (solver.cpp:28-40, its lag branch included) applied to
+// row 0 first, the segment solve (seg_solve / seg_solve_tw), the reduced
+// system by the lane scan (reduced_scan), then x = y + alpha left + beta right.
+// fail_row: -1, or a row of the first segment (or reduced pair) whose pivot
+// vanished (|piv| < 1e-300; the partition pivots stand in for Thomas's).
+template <bool TW>
+__global__ void __launch_bounds__(128) k_thomas_fast(int n, int count, const double* __restrict__ lower,
+                                                     const double* __restrict__ diag,
+                                                     const double* __restrict__ upper,
+                                                     const double* __restrict__ super2, double* rhs,
+                                                     int* fail_row) {
+    constexpr int M = 16;
+    const int line = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (line >= count) return;  // warp-uniform
+    const int t = threadIdx.x & 31;
+    const int S = (n + M - 1) / M;
+    const size_t o = static_cast<size_t>(line) * n;
+    const int a = t * M;
+    double x[M], cs[M], al[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) x[r] = a + r < n ? rhs[o + a + r] : 0.0;
+    double f0d = 1.0, f0u = 0.0;
+    if (t == 0) {
+        f0d = diag[o];
+        f0u = n > 1 ? upper[o] : 0.0;
+        const double s2 = super2[line];
+        if (s2 != 0.0 && n > 2) {
+            if (fabs(upper[o + 1]) > 1e-300) {
+                const double f = s2 / upper[o + 1];
+                f0d = fma(-f, lower[o + 1], f0d);
+                f0u = fma(-f, diag[o + 1], f0u);
+                x[0] = fma(-f, x[1], x[0]);
+            } else {  // vanishing coupling: lag the (0,2) term on the iterate
+                x[0] = fma(-s2, x[2], x[0]);
+            }
+        }
+    }
+    auto row = [&](int r, double& l, double& d, double& u) {
+        const int i = a + r;
+        if (i >= n) {
+            l = 0.0; d = 1.0; u = 0.0;
+        } else if (i == 0) {
+            l = 0.0; d = f0d; u = i == n - 1 ? 0.0 : f0u;
+        } else {
+            l = lower[o + i];
+            d = diag[o + i];
+            u = i == n - 1 ? 0.0 : upper[o + i];
+        }
+    };
+    double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
+    int bad_r = 0;
+    bool ok;
+    if constexpr (TW) ok = seg_solve_tw<M>(x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
+    else ok = seg_solve<M>(M, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
+    double lf = 0.0, rg = 0.0;
+    const int bt = reduced_scan<32>(yF, aF, bF, yL, aL, bL, t, S, lf, rg);
+    const double left = t > 0 && t < S ? lf : 0.0;
+    const double right = t < S - 1 ? rg : 0.0;
+    double b = bL;
+#pragma unroll
+    for (int r = M - 1; r >= 0; --r) {
+        if constexpr (TW) b = cs[r];
+        else if (r < M - 1) b = -cs[r] * b;
+        if (a + r < n) rhs[o + a + r] = fma(b, right, fma(al[r], left, x[r]));
+    }
+    unsigned key = 0xffffffffu;
+    if (t < S && !ok) key = static_cast<unsigned>(a + bad_r);
+    if (t < S && bt) key = min(key, static_cast<unsigned>(bt * M));
+    key = __reduce_min_sync(0xffffffffu, key);
+    if (t == 0) fail_row[line] = key == 0xffffffffu ? -1 : static_cast<int>(key);
+}
+
 // ============================================================ r-lines
 // Block = kLanesR consecutive k (same j) x S segments of M rows.
 template <int M>
 __global__ void __launch_bounds__(512) k_fx_r(BatchView v, int s) {
+    tl_begin(v, s, 1);
     extern __shared__ double red[];  // [kLanesR][S][8]
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
-    if (st.fail_step) return;
+    if (failed_before(st, s)) return;
     const int nr = v.nr, nv = v.nv, ny = v.ny;
     const int S = blockDim.y;
     const int tx = threadIdx.x, sg = threadIdx.y;
@@ -676,6 +758,7 @@ __global__ void __launch_bounds__(512) k_fx_r(BatchView v, int s) {
             col[static_cast<size_t>(r) * sr] = fma(b, right, fma(al[r], left, x[r]));
         }
     }
+    tl_end_thread(v, s, 1);
 }
 
 // ============================================================ v-lines
@@ -684,10 +767,11 @@ __global__ void __launch_bounds__(512) k_fx_r(BatchView v, int s) {
 // scans, carries the segment boundary values across segments in shared memory,
 // and fixes its rows up with the in-segment products BF/BB.
 __global__ void __launch_bounds__(512, 2) k_fx_v(BatchView v, int s) {
+    tl_begin(v, s, 2);
     extern __shared__ double car[];  // [2][S][32]
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
-    if (st.fail_step) return;
+    if (failed_before(st, s)) return;
     const int nr = v.nr, nv = v.nv, ny = v.ny;
     const int S = blockDim.y;
     const int tx = threadIdx.x, sg = threadIdx.y;
@@ -771,6 +855,7 @@ __global__ void __launch_bounds__(512, 2) k_fx_v(BatchView v, int s) {
 #pragma unroll
     for (int r = 0; r < kSegV; ++r)
         if (r < m) col[static_cast<size_t>(r) * ny] = fma(T[kFV * r + FV_BB], cout, x[r]);
+    tl_end_thread(v, s, 2);
 }
 
 // ============================================================ y-lines + update
@@ -781,10 +866,11 @@ __global__ void __launch_bounds__(512, 2) k_fx_v(BatchView v, int s) {
 // re-imposition, max|dU| and the guard (solver.cpp:151-176).
 template <int LY>
 __global__ void __launch_bounds__(256, 2) k_fx_y(BatchView v, int s) {
+    tl_begin(v, s, 3);
     __shared__ double rs[8][32][8];  // per warp, per lane: segment end rows / reduced solution
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
-    if (st.fail_step) return;
+    if (failed_before(st, s)) return;
     const int nr = v.nr, nv = v.nv, ny = v.ny;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     constexpr int LPW = 32 / LY;  // lines per warp
@@ -920,6 +1006,7 @@ __global__ void __launch_bounds__(256, 2) k_fx_y(BatchView v, int s) {
         md = y2 > md ? y2 : md;
     }
     if (lane == 0 && md) atomicMax(&st.maxdelta_bits, md);
+    tl_end_thread(v, s, 3);
 }
 
 template <int LY>
@@ -973,11 +1060,13 @@ __device__ __forceinline__ double face_entry(const BatchView& v, int p, int s, i
 }
 
 __global__ void __launch_bounds__(256) k_faces(BatchView v, int s) {
+    tl_begin(v, s, 4);
     const int p = blockIdx.y;
-    if (v.st[p].fail_step) return;
+    if (failed_before(v.st[p], s)) return;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= v.fb_stride) return;
     v.fb[static_cast<size_t>(p) * v.fb_stride + q] = face_entry(v, p, s, q);
+    tl_end_thread(v, s, 4);
 }
 
 // out-of-line slow paths (take the view by value so the kernels' own copy stays
@@ -1075,9 +1164,10 @@ __device__ __noinline__ double explicit_slow(const BatchView v, int p, int s, in
 // k edges are selects.
 template <int NV, int NY>
 __global__ void __launch_bounds__(256) k_ex4(BatchView v, int s) {
+    tl_begin(v, s, 0);
     const int p = blockIdx.z, i = blockIdx.y;
     DevStatus& st = v.st[p];
-    if (st.fail_step) return;
+    if (failed_before(st, s)) return;
     constexpr int TK = NY / 32 > 0 ? NY / 32 : 1;
     constexpr int SR = NV * NY;
     const int jt = blockIdx.x / TK;
@@ -1129,12 +1219,14 @@ __global__ void __launch_bounds__(256) k_ex4(BatchView v, int s) {
     if ((kN && dir(v, F_YMAX)) || (k0 && dir(v, F_YMIN)))
         out = v.apply_only ? 0.0 : fval(v, p, kN ? F_YMAX : F_YMIN, i, k) - u0;
     v.D[off + q] = out;
+    tl_end_thread(v, s, 0);
 }
 
 // ------------------------------------------------------------ y-lines + update
 // NY/MY lanes per line (MY contiguous rows per lane, 128-bit loads/stores).
 template <int NV, int NY, int MY>
 __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
+    tl_begin(v, s, 3);
     constexpr int kSegY = MY;
     constexpr int LY = NY / kSegY;
     constexpr int LPW = 32 / LY;
@@ -1142,7 +1234,7 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
     __shared__ double rsp[8][LY * TS + 1];           // per warp: [segment][field][line]
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
-    if (st.fail_step) return;
+    if (failed_before(st, s)) return;
     const int nr = v.nr;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int sy = lane % LY;
@@ -1298,6 +1390,7 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
     for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
     if (lane == 0 && md > 0.0)
         atomicMax(&st.maxdelta_bits, static_cast<unsigned long long>(__double_as_longlong(md)));
+    tl_end_thread(v, s, 3);
 }
 
 // ------------------------------------------------------------ pass A, fused
@@ -1343,6 +1436,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     // launched as a programmatic dependent of the previous kernel: everything
     // below reads what it wrote (no-op without a programmatic dependency)
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    tl_begin(v, s, 0);
     constexpr int M = 16;
     constexpr int SR = NV * NY;
     extern __shared__ double sm[];
@@ -1354,7 +1448,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     double* fy = rt + v.nr * kFR;              // [2][nr] y-face values (YMAX, YMIN)
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
-    const int fail = v.dbg ? 0 : st.fail_step;  // checked after the prologue loads are in flight
+    const bool fail = !v.dbg && failed_before(st, s);  // checked after the prologue loads are in flight
     const int nr = v.nr;
     const int tx = threadIdx.x, sg = threadIdx.y;
     const int tid = sg * 16 + tx;
@@ -1479,6 +1573,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             if (i == nr - 1 && rmaxD) f = rmaxv;
             dcol[static_cast<size_t>(i) * SR] = f - u0;
         }
+        tl_end(v, s, 0);
         return;
     }
 
@@ -1701,6 +1796,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         if (r < M - 1) b = -cs[r] * b;
         dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(al[r], left, x[r]));
     }
+    tl_end(v, s, 0);
 }
 
 inline size_t pa_smem(int nr) {
@@ -1759,6 +1855,7 @@ template <int NV, int NY, int CS, int NTX, int MB>
 __global__ void __launch_bounds__(NTX, (PlaneGeom<NV, NY, CS, NTX, MB>::MINB))
 k_plane(BatchView v, int s) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of pass A
+    tl_begin(v, s, 2);
     using G = PlaneGeom<NV, NY, CS, NTX, MB>;
     constexpr int MS = G::MS, LY = G::LY, SV = G::SV, SVL = G::SVL, RV = G::RV, NT = G::NT;
     extern __shared__ double sm[];
@@ -1774,8 +1871,12 @@ k_plane(BatchView v, int s) {
     const int j0 = c * RV;
     const int p = w / nr, i = w - (w / nr) * nr;
     DevStatus& st = v.st[p];
-    // a failed problem skips the work but still takes part in the cluster barriers
-    const bool live_p = v.dbg || st.fail_step == 0;
+    // a failed problem skips the work but still takes part in the cluster barriers;
+    // failed_before is uniform over the cluster (values written by earlier launches)
+    const bool live_p = v.dbg || !failed_before(st, s);
+    // distributed shared memory of a peer CTA may be written only once the whole
+    // cluster is known to be running: arrive here, wait before the first bcast
+    if constexpr (CS > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     auto cluster_sync = [] {
         if constexpr (CS > 1) cg::this_cluster().sync();
         else __syncthreads();
@@ -1849,6 +1950,7 @@ k_plane(BatchView v, int s) {
         }
     }
     __syncthreads();
+    if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     const bool planeD = (i == nr - 1 && dir(v, F_RMAX)) || (i == 0 && dir(v, F_RMIN));
     const bool yminD = dir(v, F_YMIN), ymaxD = dir(v, F_YMAX);
     const bool vminD = dir(v, F_VMIN), vmaxD = dir(v, F_VMAX);
@@ -2191,6 +2293,25 @@ k_plane(BatchView v, int s) {
             fbn[q] = (v.dmask >> face & 1) ? face_value(v.pc[p], stp, T, face, i, k) : 0.0;
         }
     }
+    tl_end(v, s, 2);
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize belongs to the device context the
+// call is made on, so it is set once per (device, kernel, size): in-process
+// multi-device batches (hjmsv_batch_run over several devices) launch the same
+// kernels on every device.
+void smem_attr(const void* fn, size_t bytes) {
+    if (bytes <= 48 * 1024) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;  // the launch reports it
+    static std::mutex mu;
+    static std::set<std::tuple<int, const void*, size_t>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({dev, fn, bytes})) return;
+    // a failure stays the pending error: the caller's cudaGetLastError reports it
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)) ==
+        cudaSuccess)
+        done.insert({dev, fn, bytes});
 }
 
 // programmatic dependent launch of the two passes (HJMSV_PDL=0 turns it off)
@@ -2220,12 +2341,7 @@ void launch_pdl(K kernel, dim3 g, dim3 b, size_t sm, cudaStream_t stream, const 
 template <int NV, int NY, int CS, int NT, int MB = 0>
 void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
     using G = PlaneGeom<NV, NY, CS, NT, MB>;
-    static const bool attr = [] {
-        cudaFuncSetAttribute(k_plane<NV, NY, CS, NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(G::SMEM));
-        return true;
-    }();
-    (void)attr;
+    smem_attr(reinterpret_cast<const void*>(k_plane<NV, NY, CS, NT, MB>), G::SMEM);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(v.nr * v.P * CS);
     cfg.blockDim = dim3(NT);
@@ -2322,27 +2438,20 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         // warps; shorter ones by warp 0's two-ended recurrence (measured faster:
         // the scan's registers make the march spill)
         const bool scan = S >= 16 && (S & (S - 1)) == 0 && !(v.dbg & 2);
-        static const bool attr = [] {
-            const int mx = static_cast<int>(pa_smem(512));
-            cudaFuncSetAttribute(k_pa<32, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_pa<64, 64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_pa<128, 128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_pa<128, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_pa<256, 256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_pa<256, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            return true;
-        }();
-        (void)attr;
+        auto go = [&](auto kern) {
+            smem_attr(reinterpret_cast<const void*>(kern), sm);
+            launch_pdl(kern, g, b, sm, stream, v, s);
+        };
         switch (shape) {
-            case 32: launch_pdl(k_pa<32, 32, false>, g, b, sm, stream, v, s); break;
-            case 64: launch_pdl(k_pa<64, 64, false>, g, b, sm, stream, v, s); break;
+            case 32: go(k_pa<32, 32, false>); break;
+            case 64: go(k_pa<64, 64, false>); break;
             case 128:
-                if (scan) launch_pdl(k_pa<128, 128, true>, g, b, sm, stream, v, s);
-                else launch_pdl(k_pa<128, 128, false>, g, b, sm, stream, v, s);
+                if (scan) go(k_pa<128, 128, true>);
+                else go(k_pa<128, 128, false>);
                 break;
             default:
-                if (scan) launch_pdl(k_pa<256, 256, true>, g, b, sm, stream, v, s);
-                else launch_pdl(k_pa<256, 256, false>, g, b, sm, stream, v, s);
+                if (scan) go(k_pa<256, 256, true>);
+                else go(k_pa<256, 256, false>);
                 break;
         }
         mark(0, "fx_explicit_sweep_r", 16.0);
@@ -2406,6 +2515,15 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
     else
         launch_y<32>(v, s, stream);
     mark(3, "fx_sweep_y_update", 24.0);
+}
+
+void fast_thomas_batch(int n, int count, const double* lower, const double* diag, const double* upper,
+                       const double* super2, double* rhs, int* fail_row, bool twisted, cudaStream_t stream) {
+    const int blocks = (count + 3) / 4;
+    if (twisted)
+        k_thomas_fast<true><<<blocks, 128, 0, stream>>>(n, count, lower, diag, upper, super2, rhs, fail_row);
+    else
+        k_thomas_fast<false><<<blocks, 128, 0, stream>>>(n, count, lower, diag, upper, super2, rhs, fail_row);
 }
 
 void fast_explicit(const BatchView& v, int s, cudaStream_t stream) {

@@ -50,7 +50,7 @@ __global__ void k_explicit(BatchView v, int s) {
     const int p = blockIdx.y;
     const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     DevStatus& st = v.st[p];
-    if (st.fail_step) return;
+    if (failed_before(st, s)) return;
     if (q == 0) st.maxdelta_bits = 0ull;
     if (q >= v.N) return;
     const int nv = v.nv, ny = v.ny, nr = v.nr;
@@ -167,7 +167,7 @@ template <int AX>
 __global__ void k_sweep(BatchView v, int s) {
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
-    if (st.fail_step) return;
+    if (failed_before(st, s)) return;
     const int nr = v.nr, nv = v.nv, ny = v.ny;
     const int lines = AX == AX_R ? nv * ny : (AX == AX_V ? nr * ny : nr * nv);
     const int line = blockIdx.x * blockDim.x + threadIdx.x;
@@ -290,7 +290,7 @@ __global__ void k_update(BatchView v, int s) {
     const int p = blockIdx.y;
     const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     DevStatus& st = v.st[p];
-    if (st.fail_step) return;  // uniform per block: p is per block
+    if (failed_before(st, s)) return;  // uniform per block: p is per block
     unsigned long long md = 0ull;
     if (q < v.N) {
         const int nv = v.nv, ny = v.ny;
@@ -405,8 +405,12 @@ void gather_spot(const BatchView& v, const long long* idx, const double* w, doub
 }
 
 void thomas_batch(int n, int count, const double* lower, const double* diag, const double* upper,
-                  const double* super2, double* rhs, double* scratch, int* fail_row, int /*fast*/,
+                  const double* super2, double* rhs, double* scratch, int* fail_row, int fast,
                   cudaStream_t stream) {
+    if (fast) {  // 1: pass A's partition solver, 2: pass B's twisted one
+        fast_thomas_batch(n, count, lower, diag, upper, super2, rhs, fail_row, fast == 2, stream);
+        return;
+    }
     k_thomas_batch<<<(count + 127) / 128, 128, 0, stream>>>(n, count, lower, diag, upper, super2,
                                                             rhs, scratch, fail_row);
 }
