@@ -1,4 +1,4 @@
-"""Per-kernel device times (CUDA events between launches) for each config.
+"""Per-kernel device times (device-clock timeline of a directly launched march) for each config.
 
     python tools/kprofile.py [--mode fast] [--configs 0,1,2,3,4] [--steps 20]
 Prints one line per kernel: average us per launch and algorithmic GB/s."""
@@ -28,8 +28,8 @@ for c in [int(x) for x in a.configs.split(",")]:
     t_create = time.time() - t0
     s.kernel_profile(2)  # warm
     s.reset()
-    prof, launches = s.kernel_profile(a.steps)
-    step_us = sum(k["avg_ms"] for k in prof) * 1e3
+    prof, launches, total_ms = s.kernel_profile(a.steps, with_total=True)
+    step_us = 1e3 * total_ms / a.steps
     pts = sum(p.size for p in probs)
     rec = {"config": c, "problems": n, "mode": a.mode, "step_us": step_us,
            "pt_steps_per_s": pts / (step_us * 1e-6), "create_s": t_create,
