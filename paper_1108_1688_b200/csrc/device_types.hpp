@@ -76,10 +76,6 @@ struct BatchView {
     // the earliest block start and the latest block end in %globaltimer ns, so
     // per-kernel durations are taken in the launch mode of the timed march
     unsigned long long* tl;
-    // L2 prefetch of the inputs of the CTA this many CTAs ahead in launch order
-    // (pass A / pass B; 0 = off): the CTA that runs next on this SM finds its
-    // HBM-resident inputs in L2
-    int pf_a, pf_b;
 };
 constexpr int kTlSlots = 5;  // 0 pass A / explicit, 1 r-lines, 2 pass B / v-lines, 3 y-lines, 4 faces
 

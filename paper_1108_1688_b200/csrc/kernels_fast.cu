@@ -1465,18 +1465,6 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const int a = sg * M;
     const size_t off = static_cast<size_t>(p) * v.N;
     const FT F = ftab(v, p);
-    if (v.pf_a) {  // the three U columns of the tile pf_a CTAs ahead -> L2 (one row per thread)
-        const long long L = static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x + v.pf_a;
-        if (L < static_cast<long long>(gridDim.x) * gridDim.y && tid < nr) {
-            const int p2 = static_cast<int>(L / gridDim.x), b2 = static_cast<int>(L % gridDim.x);
-            const int j2 = b2 / TK, kt2 = b2 - (b2 / TK) * TK;
-            const double* q = v.U + static_cast<size_t>(p2) * v.N +
-                              (static_cast<size_t>(tid) * NV + j2) * NY + kt2 * 16;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
-            if (j2 > 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(q - NY));
-            if (j2 < NV - 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(q + NY));
-        }
-    }
     // r-table and y-face values into shared memory by two bulk copies, overlapped
     // with the window prologue below
     __shared__ alignas(8) unsigned long long tbar;
@@ -1920,16 +1908,6 @@ k_plane(BatchView v, int s) {
         if (tid == 0) {  // U rows -> L2 early, so the update's loads hit L2
             constexpr unsigned bytes = RV * NY * sizeof(double);
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.U + pb), "r"(bytes) : "memory");
-            if (v.pf_b) {  // dU1 and U rows of the CTA pf_b CTAs ahead (same cluster rank)
-                const long long L = static_cast<long long>(blockIdx.x) + v.pf_b;
-                if (L < static_cast<long long>(gridDim.x)) {
-                    const int w2 = static_cast<int>(L / CS), c2 = static_cast<int>(L % CS);
-                    const int p2 = w2 / nr, i2 = w2 - (w2 / nr) * nr;
-                    const size_t pb2 = static_cast<size_t>(p2) * v.N + (static_cast<size_t>(i2) * NV + c2 * RV) * NY;
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.D + pb2), "r"(bytes) : "memory");
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.U + pb2), "r"(bytes) : "memory");
-                }
-            }
         }
         if constexpr (REGV) {
             // column segments of dU1 straight into registers (lanes = k: coalesced rows)
@@ -2418,16 +2396,6 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         w.fb_next = v0.fb + ((s + 1) & 1) * half;
     }
     w.want_md = (flags & STEP_LAST) ? 1 : 0;
-    static const int pfa_env = [] {
-        const char* e = std::getenv("HJMSV_PFA");
-        return e ? std::atoi(e) : 0;
-    }();
-    static const int pfb_env = [] {
-        const char* e = std::getenv("HJMSV_PFB");
-        return e ? std::atoi(e) : 0;
-    }();
-    w.pf_a = pfa_env;
-    w.pf_b = pfb_env;
     static const int dbg_env = [] {
         const char* e = std::getenv("HJMSV_DBG");
         return e ? std::atoi(e) : 0;
