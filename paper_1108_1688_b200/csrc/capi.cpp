@@ -428,7 +428,9 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
     h->U = dalloc<double>(PN);
     h->D = dalloc<double>(PN);
     h->U0 = dalloc<double>(PN);
-    h->C = dalloc<double>(PN);
+    // the Thomas c' scratch of the STRICT sweeps; FAST allocates it on the first
+    // readout that needs a second grid-sized buffer (Greeks / surface)
+    if (mode == HJMSV_MODE_STRICT) h->C = dalloc<double>(PN);
     h->axes = dalloc<double>(static_cast<size_t>(count) * astride);
     h->steps = dalloc<double>(static_cast<size_t>(count) * h->S * kStepStride);
     h->pc = dalloc<ProblemConst>(count);
@@ -569,6 +571,16 @@ void prof_after(void* vctx, int idx, const char* name, double b) {
     (*c->bytes)[idx] = b;
 }
 
+}  // namespace
+
+namespace {
+// one problem's second grid-sized readout buffer (FAST handles allocate it on demand)
+void ensure_scratch(hjmsv_solver* h) {
+    if (!h->C) {
+        h->C = dalloc<double>(static_cast<size_t>(h->N));
+        h->view.C = h->C;
+    }
+}
 }  // namespace
 
 extern "C" {
@@ -864,6 +876,7 @@ int32_t hjmsv_solver_greeks(hjmsv_solver* h, int32_t problem, int32_t scale_rate
         if (h->nr == 2 || h->nv == 2)
             throw Failure(HJMSV_UNSUPPORTED, "extract_greeks needs 1 or >= 3 nodes per axis");
         CK(cudaSetDevice(h->device));
+        ensure_scratch(h);
         // D / C are step workspaces, free between steps
         greeks(h->view, problem, scale_rate ? 1 : 0, h->low[problem].r0, h->D, h->C, h->stream);
         CK(cudaGetLastError());
@@ -883,6 +896,7 @@ int32_t hjmsv_solver_surface(hjmsv_solver* h, int32_t problem, int32_t k, double
         if (h->nr == 2 || h->nv == 2)
             throw Failure(HJMSV_UNSUPPORTED, "extract_greeks needs 1 or >= 3 nodes per axis");
         CK(cudaSetDevice(h->device));
+        ensure_scratch(h);
         const double r0 = h->low[problem].r0;
         greeks(h->view, problem, 1, r0, h->D, h->C, h->stream);
         const size_t rows = static_cast<size_t>(h->nr) * h->nv;
