@@ -2,6 +2,8 @@
 
     caplet_ladder(base, strikes)      instruments.cpp:238-266  one caplet per strike
     convergence(make, ...)            job.cpp:381-472          cmd_convergence's table
+    reference_caplet(payment, expiry) job.cpp:148-193          the job defaults' caplet
+    bench(cases)                      job.cpp:540-567          cmd_bench's timing table
 
 The reference fans caplet_ladder's strikes over std::threads (each a full
 price_caplet); here the strikes share mesh, model, curve and maturity, so they
@@ -20,9 +22,13 @@ import numpy as np
 
 from . import _abi as A
 from .api import _BY_CODE, HjmsvError, _check, batch_run, price
-from .problem import ProblemSpec, SolverConfig, _ptr
+from .problem import AxisSpec, ProblemSpec, SolverConfig, _ptr
 
-__all__ = ["caplet_ladder", "convergence"]
+__all__ = ["caplet_ladder", "convergence", "reference_caplet", "bench", "PAPER_BENCH_SECONDS"]
+
+# The paper's timing table: caplet, default 100x50x50 mesh,
+# 12 steps per year, wall seconds on a Pentium IV 3.2 GHz, keyed by (T_M, T).
+PAPER_BENCH_SECONDS = {(2.0, 1.0): 0.9, (11.0, 10.0): 7.3, (20.0, 19.0): 14.0}
 
 
 def caplet_ladder(base: ProblemSpec, strikes: Sequence[float], config: Optional[SolverConfig] = None,
@@ -108,4 +114,54 @@ def convergence(make: Callable[[int, int, int], ProblemSpec], nr_list: Sequence[
     for q in range(1, len(mesh_errors)):  # observed spatial order (bond sweeps halve dx)
         ratio = mesh_errors[q - 1] / max(mesh_errors[q], 1e-300)
         rows.append({"sweep": "order", "error_or_delta": math.log2(ratio)})
+    return rows
+
+
+def _discount(p: ProblemSpec, t: float) -> float:
+    cp = p.to_c()
+    tt, out = np.array([t]), np.empty(1)
+    _check(A.load().hjmsv_curve_eval(ctypes.byref(cp.curve), 0, 1, _ptr(tt), _ptr(out)))
+    return float(out[0])
+
+
+def reference_caplet(payment: float, expiry: float, strike: Optional[float] = None) -> ProblemSpec:
+    """The caplet an empty job file prices (JobConfig defaults, job.hpp:43-85):
+    flat curve 1.04 (curve.cpp:11-20), ModelParams::market_2007 (model.cpp:8-10:
+    kappa 0.001, lambda 0.15, gamma 0.9, eps 1.5, theta 0.25, rho -0.75), strike =
+    the period forward rate (job.cpp:154-166), mesh MeshSpec::caplet_default
+    (instruments.cpp:11-22: 100 x 50 x 50 sinh axes from default_axes, mesh.cpp:94-102,
+    r0 = 0.01), and run()'s own step count lround(steps_per_year * T) and time levels
+    (solver.cpp:213-258), as price_caplet builds it (instruments.cpp:210-236)."""
+    r0 = 0.01
+    base = ProblemSpec(r=AxisSpec.uniform(0, 1, 3), v=AxisSpec.uniform(0, 1, 3), y=AxisSpec.uniform(0, 1, 3),
+                       kappa=0.001, lam=0.15, gamma=0.9, eps=1.5, theta=0.25, rho=-0.75, maturity=expiry,
+                       r0=r0, flat_base=1.04)
+    if strike is None:  # period_forward_rate (job.cpp:154-157)
+        strike = (_discount(base, expiry) / _discount(base, payment) - 1.0) / (payment - expiry)
+    k = strike / r0
+    return dataclasses.replace(
+        base, r=AxisSpec.sinh(k, 0.05, 0.0, 250.0, 100), v=AxisSpec.sinh(0.5, 0.5, 0.0, 30.0, 50),
+        y=AxisSpec.sinh(0.0, 0.05, 0.0, 250.0, 50), instrument=A.INSTRUMENT_CAPLET, payment=payment,
+        strike=strike, n_steps=0, time_levels=A.TIME_REFERENCE)
+
+
+def bench(cases: Sequence[Tuple[float, float]] = ((2.0, 1.0), (11.0, 10.0), (20.0, 19.0)),
+          config: Optional[SolverConfig] = None, device: int = 0, mode: str = "fast") -> List[dict]:
+    """cmd_bench's rows (job.cpp:540-567): for each (payment, expiry) case the job
+    defaults' caplet priced end to end — lowering, terminal level + smoothing,
+    the march, the spot readout — with its wall time, beside the paper's figure."""
+    import time
+    from .api import Solver
+    rows = []
+    for payment, expiry in cases:
+        p = reference_caplet(payment, expiry)
+        t0 = time.perf_counter()
+        with Solver([p], config, device, mode) as s:
+            s.run()
+            value = float(s.spot_prices()[0])
+            n_steps = s.n_steps
+        wall = time.perf_counter() - t0
+        rows.append({"payment_years": payment, "expiry_years": expiry, "n_steps": n_steps,
+                     "wall_seconds": wall, "price": value,
+                     "paper_seconds": PAPER_BENCH_SECONDS.get((float(payment), float(expiry)))})
     return rows

@@ -53,3 +53,33 @@ def test_convergence_table_rows(gpu, oracle):
         disc = oracle.curve_eval(p, 0, np.array([p.maturity]))[0]
         assert abs(r["error_or_delta"] - abs(r["value"] - disc)) <= 1e-12
     assert np.isfinite(rows[-1]["error_or_delta"])
+
+
+def test_reference_caplet_is_the_job_default(reference):
+    """reference_caplet rebuilds price_caplet's problem for the job defaults: the
+    strike is the period forward rate, the axes are MeshSpec::caplet_default's."""
+    p = drivers.reference_caplet(11.0, 10.0)
+    assert p.shape == (100, 50, 50) and p.instrument == A.INSTRUMENT_CAPLET
+    assert p.n_steps == 0 and p.time_levels == A.TIME_REFERENCE  # run()'s own steps and levels
+    d = reference.curve_eval(p, 0, np.array([10.0, 11.0]))
+    assert p.strike == (d[0] / d[1] - 1.0) / 1.0
+    for ax, (c, a, n) in ((p.r, (p.strike / 0.01, 0.05, 100)), (p.v, (0.5, 0.5, 50)), (p.y, (0.0, 0.05, 50))):
+        z, j1, j2, _ = reference.sinh_axis(c, a, 0.0, 30.0 if n == 50 and c == 0.5 else 250.0, n)
+        assert np.array_equal(ax.z, z) and np.array_equal(ax.j1, j1) and np.array_equal(ax.j2, j2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["fast", "strict"])
+def test_bench_rows_match_reference_price_caplet(gpu, reference, mode):
+    """cmd_bench's three cases (job.cpp:540-567, paper table) on the
+    reference's own 100 x 50 x 50 sinh mesh, against the reference's run() itself."""
+    rows = drivers.bench(mode=mode)
+    assert [(r["payment_years"], r["expiry_years"]) for r in rows] == [(2.0, 1.0), (11.0, 10.0), (20.0, 19.0)]
+    assert [r["n_steps"] for r in rows] == [12, 120, 228]
+    for r in rows:
+        p = drivers.reference_caplet(r["payment_years"], r["expiry_years"])
+        g_ref, rep, _, _ = reference.run(p)  # the unmodified run() (instruments.cpp:234)
+        p_ref = reference.spot_price(p, g_ref)
+        assert rep["n_steps"] == r["n_steps"]
+        assert abs(r["price"] - p_ref) <= 1e-10 * abs(p_ref), (r, p_ref)
+        assert r["paper_seconds"] is not None and r["wall_seconds"] > 0
