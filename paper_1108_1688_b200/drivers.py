@@ -146,12 +146,18 @@ def reference_caplet(payment: float, expiry: float, strike: Optional[float] = No
 
 
 def bench(cases: Sequence[Tuple[float, float]] = ((2.0, 1.0), (11.0, 10.0), (20.0, 19.0)),
-          config: Optional[SolverConfig] = None, device: int = 0, mode: str = "fast") -> List[dict]:
+          config: Optional[SolverConfig] = None, device: int = 0, mode: str = "fast",
+          warmup: bool = True) -> List[dict]:
     """cmd_bench's rows (job.cpp:540-567): for each (payment, expiry) case the job
     defaults' caplet priced end to end — lowering, terminal level + smoothing,
-    the march, the spot readout — with its wall time, beside the paper's figure."""
+    the march, the spot readout — with its wall time, beside the paper's figure.
+    warmup: one untimed solve first, so the device context and memory pool are
+    not charged to the first case."""
     import time
     from .api import Solver
+    if warmup:
+        with Solver([reference_caplet(*cases[0])], config, device, mode) as s:
+            s.step(1)
     rows = []
     for payment, expiry in cases:
         p = reference_caplet(payment, expiry)
