@@ -7,8 +7,8 @@
  *   douglas_step(Grid3&, SpatialOperator&, dt, cfg) proj/core/include/hjmsv/solver.hpp:45-47
  *   SpatialOperator::apply_operator / assemble_line_*  discretization.hpp:154-160
  *   thomas_solve_inplace(TriDiagLine, rhs, scratch) solver.hpp:37
- *   interpolate_at(Grid3, zr, zv, zy)              instruments.hpp:80 (instruments.cpp:71-88)
- *   caplet_ladder(...)                              instruments.hpp:109 (instruments.cpp:238-266)
+ *   interpolate_at(Grid3, zr, zv, zy)              instruments.hpp:51 (instruments.cpp:71-88)
+ *   caplet_ladder(...)                              instruments.hpp:77 (instruments.cpp:238-266)
  * Because std::function cannot cross a C ABI (PdeProblem::terminal/source/observer,
  * BoundarySpec::value[6], ModelParams::*_fn), the problem is described here as
  * plain data: explicit axes, constant model parameters, curve quotes, an

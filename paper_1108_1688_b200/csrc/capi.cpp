@@ -527,7 +527,6 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         });
         CK(cudaMemcpyAsync(h->fast, fast_h, sizeof(double) * fast_n, cudaMemcpyHostToDevice, h->stream));
         CK(cudaStreamSynchronize(h->stream));
-        fast_prepare(v, h->stream);
         pt.mark("fast tables");
     }
     if (init_mode == INIT_DEVICE) {
@@ -821,7 +820,6 @@ int32_t hjmsv_solver_step(hjmsv_solver* h, int32_t steps) {
     const auto t0 = std::chrono::steady_clock::now();
     int32_t code = hjmsv_solver_step_async(h, steps);
     if (code != HJMSV_OK) return code;
-    if (h) h->wall_seconds += 0.0;
     code = hjmsv_solver_synchronize(h);
     if (h) {
         h->wall_seconds =

@@ -132,7 +132,6 @@ void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launch
 // explicit stage alone (stage test of apply_operator / dU0)
 void strict_explicit(const BatchView& v, int s, cudaStream_t stream);
 void fast_explicit(const BatchView& v, int s, cudaStream_t stream);
-void fast_prepare(const BatchView& v, cudaStream_t stream);  // builds v.fast from tables
 int fast_stride(int nr, int nv, int ny);
 bool fast_supported(int nr, int nv, int ny);
 void reset_status(const BatchView& v, cudaStream_t stream);

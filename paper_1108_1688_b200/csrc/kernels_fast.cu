@@ -2383,7 +2383,6 @@ bool fast_supported(int nr, int nv, int ny) {
 
 int fast_stride(int nr, int nv, int ny) { return fast_table_stride(nr, nv, ny); }
 
-void fast_prepare(const BatchView& v, cudaStream_t) { (void)v; }
 
 void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launches,
                const LaunchHook* hook, int flags) {
