@@ -327,7 +327,7 @@ class Marcher:
         self.solver.close()
 
 
-def timed(marcher, steps, warmup, flush, dist, clk=None):
+def timed(marcher, steps, warmup, flush, dist, clk=None, red_dev="cuda"):
     """W warm-up marches, K timed marches (clock sampler `clk` running over the
     timed ones only); returns (max-rank ms, summed pts per march)."""
     import contextlib
@@ -346,13 +346,16 @@ def timed(marcher, steps, warmup, flush, dist, clk=None):
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    t = torch.tensor([sum(times), float(marcher.done_pts)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([sum(times), float(marcher.done_pts), float(marcher.diverged)], dtype=torch.float64,
+                     device=red_dev)
     if dist:
         tmax = t.clone()
         dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
         tsum = t.clone()
         dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
+        marcher.diverged_all = int(tsum[2])
         return float(tmax[0]), float(tsum[1])
+    marcher.diverged_all = marcher.diverged
     return float(t[0]), float(t[1])
 
 
@@ -365,11 +368,20 @@ def main():
         return
 
     import torch
+    # one rank per GPU; with fewer GPUs than ranks (a test of the multi-rank path on
+    # one device) ranks share devices round-robin and the host-side reductions go
+    # over gloo, as NCCL refuses two ranks on one GPU
+    ndev = max(1, torch.cuda.device_count())
+    local = local % ndev
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world <= ndev:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    red_dev = "cuda" if dist is None or dist.get_backend() == "nccl" else "cpu"
 
     import paper_1108_1688_b200 as hj
     cs, probs, scaling = workload(args.config, rank, world)
@@ -383,7 +395,7 @@ def main():
 
     warm = max(args.warmup, 3)
     clk = ClockSampler(local)
-    total_ms, total_pts = timed(m, args.steps, warm, flush, dist, clk)
+    total_ms, total_pts = timed(m, args.steps, warm, flush, dist, clk, red_dev)
     launches = m.solver.last_launches()
     value = total_pts * args.steps / (total_ms / 1e3)
     ms_per_step = total_ms / args.steps
@@ -443,7 +455,7 @@ def main():
             el = time.perf_counter() - t0
             if it > 0:
                 e2e_t.append(el)
-        el = torch.tensor([sum(e2e_t)], dtype=torch.float64, device="cuda")
+        el = torch.tensor([sum(e2e_t)], dtype=torch.float64, device=red_dev)
         if dist:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
 
@@ -469,12 +481,12 @@ def main():
     if args.batched_config >= 0 and args.batched_config != args.config:
         bcs, bprobs, bscaling = workload(args.batched_config, rank, world)
         bm = Marcher(bprobs, local, args.mode)
-        b_ms, b_pts = timed(bm, args.steps, warm, flush, dist)
+        b_ms, b_pts = timed(bm, args.steps, warm, flush, dist, None, red_dev)
         bval = b_pts * args.steps / (b_ms / 1e3)
         batched = {"workload": f"config {args.batched_config}: {bcs.description}", "value": bval,
                    "unit": UNIT, "ms_per_step": b_ms / args.steps, "scaling": bscaling,
                    "problems_per_rank": len(bprobs), "problems_total": bcs.problems,
-                   "diverged_problems": bm.diverged,
+                   "diverged_problems": bm.diverged_all,
                    "step_equiv_frac": bval * BYTES_PER_PT_STEP / 1e9 / world / peak,
                    "gpu_launches": int(bm.solver.last_launches() * args.steps)}
         bm.close()
@@ -492,7 +504,7 @@ def main():
                 "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"config {args.config}: {cs.description}",
                            "problems_per_rank": len(probs), "mode": args.mode,
-                           "diverged_problems": m.diverged,
+                           "diverged_problems": m.diverged_all,
                            "step": "one full march (all ADI steps) per bench step",
                            "l2": "256 MiB write between timed marches; a march's own state is "
                                  "carried step to step on device"},

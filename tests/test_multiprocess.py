@@ -64,3 +64,25 @@ def test_gloo_world2_sharded_batch_matches_single_process(oracle):
     assert code == 0
     assert np.array_equal(np.array(flat), ref)
     assert tmax == 2.0
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_shard_the_batched_config(gpu):
+    """bench.py --gpus 2 relaunches itself under torch.distributed.run; the two
+    ranks (sharing the box's device when it has one) take contiguous halves of
+    config 2's 64 caplets (strong scaling, no data-path collective) and rank 0
+    prints the job's line: max-over-ranks time, the sum of both ranks' work."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--config", "2",
+                          "--steps", "1", "--warmup", "1", "--no-e2e", "--no-cpu-baseline", "--batched-config", "-1"],
+                         capture_output=True, text=True, timeout=900, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["problems_per_rank"] == 32
+    # all 64 caplets' steps counted (problem 41 diverges at step 372 in both solvers)
+    assert line["value"] > 0 and line["gpu_launches"] > 0
