@@ -508,7 +508,10 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         for (int p = 1; p < count; ++p)
             if ((pcs[p].rule[f] == RULE_DIRICHLET) != dir)
                 throw std::invalid_argument("batched problems must share face rules");
-        if (dir) v.dmask |= 1 << f;
+        // is_dirichlet / dirichlet_value ignore the faces of a singleton axis
+        // (discretization.cpp:153-192: r_.n > 1, v_.n > 1, y_.n > 1)
+        const int n_axis = f < 2 ? h->nr : (f < 4 ? h->nv : h->ny);
+        if (dir && n_axis > 1) v.dmask |= 1 << f;
     }
     h->stage = ov != nullptr;
     if (mode == HJMSV_MODE_FAST) {

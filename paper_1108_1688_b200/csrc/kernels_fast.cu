@@ -154,7 +154,9 @@ __global__ void __launch_bounds__(256) k_fx_explicit(BatchView v, int s) {
                 acc = fma(g1s, (up + dn) - 2.0 * u0, acc);
                 acc = fma(g4h, up - dn, acc);
             }
-            if (j == 0) {
+            if (nv == 1) {
+                // a collapsed v axis has no v terms (apply_operator, discretization.cpp:336)
+            } else if (j == 0) {
                 acc = fma(2.0 * V[FV_G5], u[ny] - u0, acc);
             } else {
                 const double up = u[ny], dn = u[-ny];
@@ -2376,8 +2378,10 @@ int specialised_shape(const BatchView& v) {
 }
 
 bool fast_supported(int nr, int nv, int ny) {
-    // collapsed axes are served by STRICT; segment counts bounded by the block shapes
-    return nr >= 3 && nv >= 3 && ny >= 3 && (nr + kSegR - 1) / kSegR <= 32 &&
+    // a collapsed v axis (price_zcb's default mesh, instruments.cpp:140-143) runs the
+    // four-kernel schedule without its v sweep; other collapsed axes are served by
+    // STRICT; segment counts bounded by the block shapes
+    return nr >= 3 && (nv >= 3 || nv == 1) && ny >= 3 && (nr + kSegR - 1) / kSegR <= 32 &&
            (nv + kSegV - 1) / kSegV <= 16 && ny <= 32 * kSegY;
 }
 
@@ -2480,9 +2484,11 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         mark(2, "fx_plane_vy_update", 24.0);
         return;
     }
-    const int Sv = (v.nv + kSegV - 1) / kSegV;
-    k_fx_v<<<dim3(v.nr * tk, v.P), dim3(32, Sv), 2ull * Sv * 32 * sizeof(double), stream>>>(v, s);
-    mark(2, "fx_sweep_v", 16.0);
+    if (v.nv > 1) {  // douglas_step skips the v sweep of a collapsed v axis (solver.cpp:136)
+        const int Sv = (v.nv + kSegV - 1) / kSegV;
+        k_fx_v<<<dim3(v.nr * tk, v.P), dim3(32, Sv), 2ull * Sv * 32 * sizeof(double), stream>>>(v, s);
+        mark(2, "fx_sweep_v", 16.0);
+    }
     const int ly = (v.ny + kSegY - 1) / kSegY;
     const int lines = v.nr * v.nv;
     static const int ymy = [] {

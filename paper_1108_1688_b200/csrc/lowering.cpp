@@ -377,7 +377,9 @@ std::vector<double> build_fast_tables(const Lowered& L, const hjmsv_solver_confi
     const double inv_dxv2 = nv > 1 ? 1.0 / (dxv * dxv) : 0.0;
     const double inv_2dxv = nv > 1 ? 0.5 / dxv : 0.0;
     const double inv_2dxy = ny > 1 ? 0.5 / dxy : 0.0;
-    const double inv_cross = 0.25 / (dxr * dxv);
+    // the cross term needs both axes resolved (apply_operator applies it only for
+    // 0 < i < nr-1, 0 < j < nv-1, discretization.cpp:357-361); a singleton v axis has none
+    const double inv_cross = (nr > 1 && nv > 1) ? 0.25 / (dxr * dxv) : 0.0;
     const ProblemConst& pc = L.pc;
     const double* a = L.axes.data() + 3 * nr + 3 * nv + 3 * ny;
     const double* b = a + nr;

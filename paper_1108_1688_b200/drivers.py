@@ -3,6 +3,7 @@
     caplet_ladder(base, strikes)      instruments.cpp:238-266  one caplet per strike
     convergence(make, ...)            job.cpp:381-472          cmd_convergence's table
     reference_caplet(payment, expiry) job.cpp:148-193          the job defaults' caplet
+    reference_zcb(maturity)           instruments.cpp:173-208  price_zcb's default (collapsed v)
     bench(cases)                      job.cpp:540-567          cmd_bench's timing table
 
 The reference fans caplet_ladder's strikes over std::threads (each a full
@@ -24,7 +25,7 @@ from . import _abi as A
 from .api import _BY_CODE, HjmsvError, _check, batch_run, price
 from .problem import AxisSpec, ProblemSpec, SolverConfig, _ptr
 
-__all__ = ["caplet_ladder", "convergence", "reference_caplet", "bench", "PAPER_BENCH_SECONDS"]
+__all__ = ["caplet_ladder", "convergence", "reference_caplet", "reference_zcb", "bench", "PAPER_BENCH_SECONDS"]
 
 # The paper's timing table: caplet, default 100x50x50 mesh,
 # 12 steps per year, wall seconds on a Pentium IV 3.2 GHz, keyed by (T_M, T).
@@ -143,6 +144,25 @@ def reference_caplet(payment: float, expiry: float, strike: Optional[float] = No
         base, r=AxisSpec.sinh(k, 0.05, 0.0, 250.0, 100), v=AxisSpec.sinh(0.5, 0.5, 0.0, 30.0, 50),
         y=AxisSpec.sinh(0.0, 0.05, 0.0, 250.0, 50), instrument=A.INSTRUMENT_CAPLET, payment=payment,
         strike=strike, n_steps=0, time_levels=A.TIME_REFERENCE)
+
+
+def reference_zcb(maturity: float) -> ProblemSpec:
+    """The bond an empty job file prices with instrument = zcb: flat curve 1.04,
+    ModelParams::market_2007, MeshSpec::zcb_default(f(0,0), r0 = 0.01)
+    (instruments.cpp:24-35: 100 sinh r nodes centred on the spot rate, 40 sinh y
+    nodes) and price_zcb's collapsed v axis (the singleton v = 0 plane,
+    instruments.cpp:140-143) — a 100 x 1 x 40 grid, run()'s own step count and
+    time levels."""
+    r0 = 0.01
+    base = ProblemSpec(r=AxisSpec.uniform(0, 1, 3), v=AxisSpec.singleton(0.0), y=AxisSpec.uniform(0, 1, 3),
+                       kappa=0.001, lam=0.15, gamma=0.9, eps=1.5, theta=0.25, rho=-0.75, maturity=maturity,
+                       r0=r0, flat_base=1.04)
+    cp = base.to_c()
+    t, f0 = np.array([0.0]), np.empty(1)
+    _check(A.load().hjmsv_curve_eval(ctypes.byref(cp.curve), 1, 1, _ptr(t), _ptr(f0)))  # forward(0)
+    return dataclasses.replace(base, r=AxisSpec.sinh(float(f0[0]) / r0, 0.05, 0.0, 25.0, 100),
+                               y=AxisSpec.sinh(0.0, 0.5, 0.0, 250.0, 40), n_steps=0,
+                               time_levels=A.TIME_REFERENCE)
 
 
 def bench(cases: Sequence[Tuple[float, float]] = ((2.0, 1.0), (11.0, 10.0), (20.0, 19.0)),

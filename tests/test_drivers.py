@@ -83,3 +83,25 @@ def test_bench_rows_match_reference_price_caplet(gpu, reference, mode):
         assert rep["n_steps"] == r["n_steps"]
         assert abs(r["price"] - p_ref) <= 1e-10 * abs(p_ref), (r, p_ref)
         assert r["paper_seconds"] is not None and r["wall_seconds"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("maturity", [1.0, 10.0, 20.0])
+def test_collapsed_v_axis_runs_fast_and_matches_reference(gpu, reference, maturity):
+    """price_zcb's default mesh (100 x 1 x 40, collapsed v axis; instruments.cpp:140-143,
+    173-208) on the FAST four-kernel schedule without its v sweep (solver.cpp:136),
+    against the reference's run() on the same problem, and the SPEC acceptance bound
+    against the closed form (< 1e-5)."""
+    p = drivers.reference_zcb(maturity)
+    assert p.shape == (100, 1, 40)
+    with hj.Solver([p], mode="fast") as s:
+        s.run()
+        price = float(s.spot_prices()[0])
+        g = s.grid(0)
+        assert s.last_launches() >= 3 * s.n_steps  # explicit, r-lines, y-lines: no v sweep
+    g_ref, rep, _, _ = reference.run(p)
+    p_ref = reference.spot_price(p, g_ref)
+    assert abs(price - p_ref) <= 1e-10 * abs(p_ref), (price, p_ref)
+    assert np.max(np.abs(g - g_ref)) <= 1e-10 * np.max(np.abs(g_ref))
+    disc = reference.curve_eval(p, 0, np.array([maturity]))[0]
+    assert abs(price - disc) < 1e-5

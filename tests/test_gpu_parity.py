@@ -4,6 +4,8 @@ Bar (BASELINE north_star): |p_gpu - p_ref| <= 1e-10 |p_ref| and
 max|U_gpu - U_ref| <= 1e-10 max|U_ref|, per problem, FP64. STRICT mode keeps
 the reference's operation order, so it is held to a tighter 1e-13 on grids.
 """
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -331,7 +333,8 @@ def test_get_grids_matches_get_grid(gpu):
 def test_collapsed_v_axis_zcb(gpu, oracle):
     """price_zcb's collapsed mesh (singleton v axis, instruments.cpp:134-143): the
     SPEC.md acceptance case (flat 4%, T=20, 100x40, 12 steps/yr) on the device.
-    STRICT serves collapsed axes; FAST reports UNSUPPORTED."""
+    STRICT and FAST (four-kernel schedule without the v sweep) both serve it;
+    other collapsed axes are STRICT-only and FAST reports UNSUPPORTED."""
     import math
     spot = math.log(1.04)
     rax = AxisSpec.sinh(spot / 0.01, 0.05, 0.0, 25.0, 100)
@@ -348,8 +351,13 @@ def test_collapsed_v_axis_zcb(gpu, oracle):
     assert rep_ref["n_steps"] == 240
     assert abs(price - oracle.interpolate(p, g_ref, spot / 0.01, 0.0, 0.0)) <= 1e-12
     assert abs(price - 1.04 ** -20) < 1e-5  # SPEC.md:525 acceptance
+    with hj.Solver([p], mode="fast") as s:
+        s.run()
+        assert B.normwise_rel(s.grid(0), g_ref) <= TOL
+        assert abs(s.price(0, spot / 0.01, 0.0, 0.0) - price) <= 1e-10 * price
+    py = dataclasses.replace(p, v=AxisSpec.sinh(0.5, 0.5, 0.0, 30.0, 8), y=AxisSpec.singleton(0.0))
     with pytest.raises(hj.Unsupported):
-        hj.Solver([p], mode="fast")
+        hj.Solver([py], mode="fast")
 
 
 @pytest.mark.parametrize("mode", MODES)
