@@ -133,3 +133,42 @@ def test_solver_requires_a_device_here():
     p = W.make_problem(0, 0, nr=8, nv=4, ny=4, steps=4)
     with pytest.raises(hj.CudaError):
         hj.Solver([p])
+
+
+def test_fast_lines_are_bounded_and_modes_validated():
+    """hjmsv_thomas_batch: FAST lines hold at most 32 segments of 16 rows (n <= 512);
+    an unknown mode is an invalid argument. Both are decided before any device work."""
+    import numpy as np
+    import paper_1108_1688_b200 as hj
+    n, c = 600, 2
+    z = np.zeros((c, n))
+    d = np.ones((c, n))
+    with pytest.raises(hj.Unsupported):
+        hj.thomas_batch(z, d, z, np.zeros(c), d, mode="fast")
+    with pytest.raises(hj.Unsupported):
+        hj.thomas_batch(z, d, z, np.zeros(c), d, mode="fast_twisted")
+    with pytest.raises(hj.InvalidArgument):
+        hj.thomas_batch(z[:, :8], d[:, :8], z[:, :8], np.zeros(c), d[:, :8], mode=7)
+
+
+@pytest.mark.gpu
+def test_kernel_timeline_shares(gpu):
+    """hjmsv_solver_kernel_timeline: per-kernel durations from the device clock of
+    every block in a march launched like the timed one; the per-step kernels'
+    durations add up to at most the march (no overlap is counted twice)."""
+    import paper_1108_1688_b200 as hj
+    from paper_1108_1688_b200 import workloads as W
+    p = W.make_problem(1, 0, steps=40)
+    with hj.Solver([p], mode="fast") as s:
+        prof, launches, total_ms = s.kernel_profile(40, with_total=True)
+        names = [k["name"] for k in prof]
+        assert "fx_explicit_sweep_r" in names and "fx_plane_vy_update" in names
+        per_step = sum(k["avg_ms"] for k in prof if k["name"] != "fx_faces") * 40
+        assert 0.5 * total_ms < per_step <= 1.0 * total_ms
+        assert launches >= 80
+        alg = {k["name"]: k["alg_bytes"] for k in prof}
+        assert alg["fx_explicit_sweep_r"] == 16.0 * p.size and alg["fx_plane_vy_update"] == 24.0 * p.size
+        with pytest.raises(hj.InvalidArgument):
+            s.kernel_profile(1)  # the march is over: reset first
+        s.reset()
+        s.kernel_profile(2)
