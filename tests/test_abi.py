@@ -160,6 +160,10 @@ def test_kernel_timeline_shares(gpu):
     from paper_1108_1688_b200 import workloads as W
     p = W.make_problem(1, 0, steps=40)
     with hj.Solver([p], mode="fast") as s:
+        # the first profiled sequence of a fresh process also pays module loading
+        # and first-touch costs inside its event-timed total: warm up once
+        s.kernel_profile(40)
+        s.reset()
         prof, launches, total_ms = s.kernel_profile(40, with_total=True)
         names = [k["name"] for k in prof]
         assert "fx_explicit_sweep_r" in names and "fx_plane_vy_update" in names
