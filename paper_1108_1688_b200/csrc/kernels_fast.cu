@@ -1433,7 +1433,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int NV, int NY, bool SCAN>
+template <int NV, int NY, bool SCAN, int KL = 16, int TPC = 1>
 __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     // launched as a programmatic dependent of the previous kernel: everything
     // below reads what it wrote (no-op without a programmatic dependency)
@@ -1443,27 +1443,36 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     constexpr int SR = NV * NY;
     extern __shared__ double sm[];
     const int S = blockDim.y;
-    const int nt = 16 * S;
-    double* red = sm;                          // [16][8S+9] reduced-system rows
-    double* ring = red + 16 * (8 * S + 9);     // [nt][kRing*4 + 1] window prefetch (padded)
-    double* rt = ring + (kRing * 4 + 1) * nt;  // [nr][8] r-table (FastR)
+    // KL consecutive k per segment group (16: one CTA of 16 S threads per SM on
+    // 512-row lines; 8: two co-resident CTAs of 8 S threads — measured slower)
+    static_assert(KL == 16 || KL == 8, "k-lane group");
+    // TPC column tiles (KL consecutive k of one j) per CTA, marched one after the
+    // other: the next tile's window and ring rows are queued (cp.async into the
+    // thread's staging slots) as soon as a tile's march ends, so their latency
+    // hides behind that tile's reduced systems and writes; per-CTA setup (tables,
+    // r-table bulk copy) is paid once per TPC tiles
+    static_assert(TPC == 1 || TPC == 2, "tiles per CTA");
+    constexpr bool STAGE = TPC > 1;
+    constexpr int RST = kRing * 4 + (STAGE ? 12 : 0) + 1;  // per-thread ring (+ window staging) stride
+    const int nt = KL * S;
+    double* red = sm;                          // [KL][8S+9] reduced-system rows
+    double* ring = red + KL * (8 * S + 9);     // [nt][RST] window prefetch (padded)
+    double* rt = ring + RST * nt;              // [nr][8] r-table (FastR)
     double* fy = rt + v.nr * kFR;              // [2][nr] y-face values (YMAX, YMIN)
     const int p = blockIdx.y;
     DevStatus& st = v.st[p];
     const bool fail = !v.dbg && failed_before(st, s);  // checked after the prologue loads are in flight
     const int nr = v.nr;
     const int tx = threadIdx.x, sg = threadIdx.y;
-    const int tid = sg * 16 + tx;
-    constexpr int TK = NY / 16;
-    const int j = blockIdx.x / TK;
-    const int k = (blockIdx.x - j * TK) * 16 + tx;
+    const int tid = sg * KL + tx;
+    constexpr int TK = NY / KL;
+    static_assert(TK % TPC == 0, "the tiles of a CTA share j");
+    const int j = (blockIdx.x * TPC) / TK;
+    const int kt0 = blockIdx.x * TPC - j * TK;  // first k tile of this CTA
     const ProblemConst& pc = v.pc[p];
     const bool yminD = dir(v, F_YMIN), ymaxD = dir(v, F_YMAX);
-    const bool k0 = k == 0, kN = k == NY - 1;
-    const unsigned hmask = 0xffffu << ((sg & 1) * 16);  // this half-warp (blockDim.x == 16)
-    // is_dirichlet(1,j,k) (solver.cpp:127): the column lies on a v or y Dirichlet face
-    const bool solve = !(kN && ymaxD) && !(j == NV - 1 && dir(v, F_VMAX)) && !(k0 && yminD) &&
-                       !(j == 0 && dir(v, F_VMIN));
+    // this KL-lane group of the warp (blockDim.x == KL)
+    const unsigned hmask = (KL == 16 ? 0xffffu : 0xffu) << ((sg & (32 / KL - 1)) * KL);
     const int a = sg * M;
     const size_t off = static_cast<size_t>(p) * v.N;
     const FT F = ftab(v, p);
@@ -1481,10 +1490,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const double2* V2 = reinterpret_cast<const double2*>(F.V + kFV * j);
     double2 v01 = __ldg(V2);
     const double2 v23 = __ldg(V2 + 1);  // (V, G2), (G5, G3V)
-    const double2* Y2 = reinterpret_cast<const double2*>(F.Y + kFY * k);
-    const double2 y01 = __ldg(Y2), y23 = __ldg(Y2 + 1);  // (S6, T6), (Y, pad)
-    const double vj = v01.x, yk = y23.x;
-    const double vs6 = vj * y01.x, t6 = y01.y;
+    const double vj = v01.x;
     const double th = pc.theta_dt, dtm = pc.dt;
     const bool rmaxD = dir(v, F_RMAX), rminD = dir(v, F_RMIN);
     // v-face rows (block-uniform): j = nv-1 is the v_max Dirichlet face (an early,
@@ -1500,12 +1506,40 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     if (jdeg) v01.y = v23.x;
     const bool order2y = v.y_order != 1, order2r = v.r_order != 1;
     const double* fbp = v.fb + static_cast<size_t>(p) * v.fb_stride;
-    const double* fyk = fy + (kN ? 0 : nr);
-    const bool kface = (kN && ymaxD) || (k0 && yminD);
-    // r-face values this thread needs (first / last segment), loaded up front
-    const double rminv = (sg == 0 && rminD) ? __ldg(fbp + NY + k) : 0.0;
-    const double rmaxv = (a + M == nr && rmaxD) ? __ldg(fbp + k) : 0.0;
-    const double* __restrict__ col = v.U + off + static_cast<size_t>(j) * NY + k;
+
+    // ---- per-tile (k-dependent) state, set by tile_setup(t)
+    int k = 0;
+    bool k0 = false, kN = false, solve = false, kface = false, edge = false;
+    int eoff = 0;
+    double yk = 0.0, vs6 = 0.0, t6 = 0.0, ths = 0.0, rminv = 0.0, rmaxv = 0.0;
+    const double* fyk = fy;
+    const double* __restrict__ col = v.U;
+    auto tile_k = [&](int t) { return (kt0 + t) * KL + tx; };
+    auto tile_setup = [&](int t) {
+        k = tile_k(t);
+        k0 = k == 0;
+        kN = k == NY - 1;
+        // is_dirichlet(1,j,k) (solver.cpp:127): the column lies on a v or y Dirichlet face
+        solve = !(kN && ymaxD) && !(j == NV - 1 && dir(v, F_VMAX)) && !(k0 && yminD) && !(j == 0 && dir(v, F_VMIN));
+        const double2* Y2 = reinterpret_cast<const double2*>(F.Y + kFY * k);
+        const double2 y01 = __ldg(Y2), y23 = __ldg(Y2 + 1);  // (S6, T6), (Y, pad)
+        yk = y23.x;
+        vs6 = vj * y01.x;
+        t6 = y01.y;
+        fyk = fy + (kN ? 0 : nr);
+        kface = (kN && ymaxD) || (k0 && yminD);
+        // r-face values this thread needs (first / last segment)
+        rminv = (sg == 0 && rminD) ? __ldg(fbp + NY + k) : 0.0;
+        rmaxv = (a + M == nr && rmaxD) ? __ldg(fbp + k) : 0.0;
+        col = v.U + off + static_cast<size_t>(j) * NY + k;
+        // the KL-lane group's edge lanes also carry their outside neighbour in k
+        // (k-1 at tx 0, k+1 at tx KL-1; k+2 at k = 0 for the one-sided row)
+        edge = tx == 0 || (tx == KL - 1 && !kN);
+        eoff = tx == 0 ? (k0 ? 2 : -1) : 1;
+        // interior rows (0 < i < nr-1); a column that is not solved runs identity rows
+        ths = solve ? th : 0.0;
+    };
+    tile_setup(0);
     double x[M], cs[M], al[M];
     // window for columns j-1 (0), j (1), j+1 (2): m = row ic-1, c = ic, p = ic+1;
     // rows ic+2 .. ic+1+kRing are in flight in this thread's ring slots (groups 1..kRing)
@@ -1513,17 +1547,27 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     // cross term needs only that), saving two registers in the march
     double mx = 0.0, m1 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, p0 = 0.0, p1 = 0.0, p2 = 0.0;
     double ce = 0.0, pe = 0.0;
-    auto gptr = [&](int ii) { return col + static_cast<size_t>(min(max(ii, 0), nr - 1)) * SR; };
-    // this thread's ring slots: 17-double stride between threads (conflict-free),
-    // compile-time offsets inside
-    double* const myring = ring + tid * (kRing * 4 + 1);
+    auto gptr_c = [&](const double* cb, int ii) { return cb + static_cast<size_t>(min(max(ii, 0), nr - 1)) * SR; };
+    auto gptr = [&](int ii) { return gptr_c(col, ii); };
+    // this thread's ring slots (odd stride between threads, compile-time offsets
+    // inside); STAGE: 12 more slots hold the next tile's window rows
+    double* const myring = ring + tid * RST;
     const unsigned myring_s = static_cast<unsigned>(__cvta_generic_to_shared(myring));
     auto slot = [&](int q, int c) { return myring + q * 4 + c; };
-    // the 16-lane group's edge lanes also carry their outside neighbour in k
-    // (k-1 at tx 0, k+1 at tx 15; k+2 at k = 0 for the one-sided row)
-    const bool edge = tx == 0 || (tx == 15 && !kN);
-    const int eoff = tx == 0 ? (k0 ? 2 : -1) : 1;
+    auto wslot = [&](int q, int c) { return myring + kRing * 4 + q * 4 + c; };
     // the j-1 column offset is a compile-time constant in each instantiation
+    auto ring_rows = [&](auto jd, const double* cb, bool ed, int eo) {
+        constexpr int OFFM = decltype(jd)::value ? NY : -NY;
+#pragma unroll
+        for (int r = 0; r < kRing; ++r) {
+            const double* g = gptr_c(cb, a + 2 + r);
+            cp_async8s(myring_s + 8 * (r * 4 + 0), g + OFFM);
+            cp_async8s(myring_s + 8 * (r * 4 + 1), g);
+            cp_async8s(myring_s + 8 * (r * 4 + 2), g + NY);
+            if (ed) cp_async8s(myring_s + 8 * (r * 4 + 3), g + eo);
+            cp_async_commit();
+        }
+    };
     auto prologue = [&](auto jd) {
         constexpr int OFFM = decltype(jd)::value ? NY : -NY;
         const double* q = gptr(a - 1);
@@ -1535,19 +1579,41 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         q = gptr(a + 1);
         p0 = __ldg(q + OFFM); p1 = __ldg(q); p2 = __ldg(q + NY);
         if (edge) pe = __ldg(q + eoff);
+        ring_rows(jd, col, edge, eoff);
+    };
+    // STAGE: the window rows a-1, a, a+1 of the tile at cb as one cp.async group
+    // into the staging slots, then its ring rows (kRing groups)
+    auto prologue_staged = [&](auto jd, const double* cb, bool ed, int eo) {
+        constexpr int OFFM = decltype(jd)::value ? NY : -NY;
+        const unsigned ws = myring_s + 8 * (kRing * 4);
 #pragma unroll
-        for (int r = 0; r < kRing; ++r) {
-            const double* g = gptr(a + 2 + r);
-            cp_async8s(myring_s + 8 * (r * 4 + 0), g + OFFM);
-            cp_async8s(myring_s + 8 * (r * 4 + 1), g);
-            cp_async8s(myring_s + 8 * (r * 4 + 2), g + NY);
-            if (edge) cp_async8s(myring_s + 8 * (r * 4 + 3), g + eoff);
-            cp_async_commit();
+        for (int w = 0; w < 3; ++w) {
+            const double* g = gptr_c(cb, a - 1 + w);
+            cp_async8s(ws + 8 * (w * 4 + 0), g + OFFM);
+            cp_async8s(ws + 8 * (w * 4 + 1), g);
+            cp_async8s(ws + 8 * (w * 4 + 2), g + NY);
+            if (w > 0 && ed) cp_async8s(ws + 8 * (w * 4 + 3), g + eo);
         }
+        cp_async_commit();
+        ring_rows(jd, cb, ed, eo);
+    };
+    auto window_from_stage = [&] {
+        cp_async_wait<kRing>();  // the staging group (the ring groups may be in flight)
+        m1 = *wslot(0, 1);
+        mx = *wslot(0, 2) - *wslot(0, 0);
+        c0 = *wslot(1, 0); c1 = *wslot(1, 1); c2 = *wslot(1, 2);
+        if (edge) ce = *wslot(1, 3);
+        p0 = *wslot(2, 0); p1 = *wslot(2, 1); p2 = *wslot(2, 2);
+        if (edge) pe = *wslot(2, 3);
     };
     if (!jdir) {
-        if (jdeg) prologue(std::true_type{});
-        else prologue(std::false_type{});
+        if constexpr (STAGE) {
+            if (jdeg) prologue_staged(std::true_type{}, col, edge, eoff);
+            else prologue_staged(std::false_type{}, col, edge, eoff);
+        } else {
+            if (jdeg) prologue(std::true_type{});
+            else prologue(std::false_type{});
+        }
     }
     __syncthreads();  // the mbarrier is initialised
     bulk_wait(tbar_s);  // rt, fy have landed
@@ -1560,20 +1626,24 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         // a Dirichlet v face: every column is an identity line, dU1 = dU0 =
         // face(t_next) - U (solver.cpp:111-116, 127), with the face precedence
         // r_max > y_max > v_max > r_min > y_min > v_min (discretization.cpp:153-192)
-        const double* fv = fbp + 2 * NY + 2 * nr + (jhi ? 0 : nr * NY) + k;
-        double* dcol = v.D + off + static_cast<size_t>(j) * NY + k;
+#pragma unroll 1
+        for (int t = 0; t < TPC; ++t) {
+            if (t > 0) tile_setup(t);
+            const double* fv = fbp + 2 * NY + 2 * nr + (jhi ? 0 : nr * NY) + k;
+            double* dcol = v.D + off + static_cast<size_t>(j) * NY + k;
 #pragma unroll 4
-        for (int r = 0; r < M; ++r) {
-            const int i = a + r;
-            const double u0 = __ldg(col + static_cast<size_t>(i) * SR);
-            double f = __ldg(fv + static_cast<size_t>(i) * NY);
-            if (!jhi) {  // v_min ranks last
-                if (i == 0 && rminD) f = rminv;
-                if (k0 && yminD) f = fyk[i];
+            for (int r = 0; r < M; ++r) {
+                const int i = a + r;
+                const double u0 = __ldg(col + static_cast<size_t>(i) * SR);
+                double f = __ldg(fv + static_cast<size_t>(i) * NY);
+                if (!jhi) {  // v_min ranks last
+                    if (i == 0 && rminD) f = rminv;
+                    if (k0 && yminD) f = fyk[i];
+                }
+                if (kN && ymaxD) f = fyk[i];
+                if (i == nr - 1 && rmaxD) f = rmaxv;
+                dcol[static_cast<size_t>(i) * SR] = f - u0;
             }
-            if (kN && ymaxD) f = fyk[i];
-            if (i == nr - 1 && rmaxD) f = rmaxv;
-            dcol[static_cast<size_t>(i) * SR] = f - u0;
         }
         tl_end(v, s, 0);
         return;
@@ -1599,8 +1669,6 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             u = -(w2 + w1);
         }
     };
-    // interior rows (0 < i < nr-1); a column that is not solved runs identity rows
-    const double ths = solve ? th : 0.0;
     auto interior = [&](double g1s, double g4h, double& l, double& d, double& u) {
         const double w2 = ths * g1s, w1 = ths * g4h;
         l = w1 - w2;
@@ -1616,194 +1684,217 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         return fma(c4, r01.y, fma(r23.y, yk, fma(r45.x, vj, r23.x)));
     };
 
-    double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
-    int bad_r = 0;
-    bool ok = true;
-    auto march = [&](auto jd) {
-        constexpr int OFFM = decltype(jd)::value ? NY : -NY;
-        // window for columns j-1 (0), j (1), j+1 (2): m = row ic-1, c = ic, p = ic+1;
-        // rows ic+2 .. ic+1+kRing are in flight in this thread's ring slots
-        // centre moves to row a+r: row a+r+1 comes out of ring slot (r-1) % kRing,
-        // which is refilled with row a+r+kRing+1
-        auto shift = [&](int r) {
-            const int q = (r - 1) % kRing;
-            cp_async_wait<kRing - 1>();
-            mx = c2 - c0;
-            m1 = c1;
-            c0 = p0; c1 = p1; c2 = p2; ce = pe;
-            p0 = *slot(q, 0); p1 = *slot(q, 1); p2 = *slot(q, 2);
-            if (edge) pe = *slot(q, 3);
-            const double* g = gptr(a + r + kRing + 1);
-            cp_async8s(myring_s + 8 * (q * 4 + 0), g + OFFM);
-            cp_async8s(myring_s + 8 * (q * 4 + 1), g);
-            cp_async8s(myring_s + 8 * (q * 4 + 2), g + NY);
-            if (edge) cp_async8s(myring_s + 8 * (q * 4 + 3), g + eoff);
-            cp_async_commit();
+    const int FS = S + 1, CST = 8 * S + 9;
+#pragma unroll 1
+    for (int t = 0; t < TPC; ++t) {
+        if (t > 0) tile_setup(t);
+        if constexpr (STAGE) window_from_stage();
+        double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
+        int bad_r = 0;
+        bool ok = true;
+        auto march = [&](auto jd) {
+            constexpr int OFFM = decltype(jd)::value ? NY : -NY;
+            // window for columns j-1 (0), j (1), j+1 (2): m = row ic-1, c = ic, p = ic+1;
+            // rows ic+2 .. ic+1+kRing are in flight in this thread's ring slots
+            // centre moves to row a+r: row a+r+1 comes out of ring slot (r-1) % kRing,
+            // which is refilled with row a+r+kRing+1 while that row lies in the
+            // segment's window (rows up to a+M); later shifts only drain the ring
+            auto shift = [&](int r) {
+                const int q = (r - 1) % kRing;
+                if (r <= M - kRing) cp_async_wait<kRing - 1>();
+                else if (r == M - 2) cp_async_wait<1>();
+                else cp_async_wait<0>();
+                mx = c2 - c0;
+                m1 = c1;
+                c0 = p0; c1 = p1; c2 = p2; ce = pe;
+                p0 = *slot(q, 0); p1 = *slot(q, 1); p2 = *slot(q, 2);
+                if (edge) pe = *slot(q, 3);
+                if (r + kRing + 1 <= M) {
+                    const double* g = gptr(a + r + kRing + 1);
+                    {
+                    cp_async8s(myring_s + 8 * (q * 4 + 0), g + OFFM);
+                    cp_async8s(myring_s + 8 * (q * 4 + 1), g);
+                    cp_async8s(myring_s + 8 * (q * 4 + 2), g + NY);
+                    if (edge) cp_async8s(myring_s + 8 * (q * 4 + 3), g + eoff);
+                    }
+                    cp_async_commit();
+                }
+            };
+            // y-direction terms and the k faces (discretization.cpp:340-352)
+            // full: every lane of the warp is here (rows r >= 1); row 0 runs the
+            // face-row code in lane group 0 of warp 0 only, so it shuffles per group
+            auto yterm = [&](bool full, double u0, double acc, double a_i, double ed) {
+                const unsigned msk = full ? 0xffffffffu : hmask;
+                double kl = __shfl_up_sync(msk, u0, 1, KL);
+                double kr = __shfl_down_sync(msk, u0, 1, KL);
+                if (tx == 0 && !k0) kl = ed;
+                if (tx == KL - 1 && !kN) kr = ed;
+                double yd = kr - kl;
+                if (k0)  // one-sided y row (discretization.cpp:346-352); ed = U(i, j, 2)
+                    yd = order2y ? fma(4.0, kr, -ed) - 3.0 * u0 : 2.0 * (kr - u0);
+                acc = fma(fma(a_i, vs6, t6), yd, acc);
+                return acc * dtm;  // y-face Dirichlet columns are fixed up after the march
+            };
+            // dU0 at an interior row i from a window (mm, cc, pp)
+            auto stencil = [&](bool full, const double2& r01, const double2& r45, const double2& r67,
+                               double g4h, double mqx, double mq1, double cq0, double cq1,
+                               double cq2, double pq0, double pq1, double pq2, double ed) {
+                const double u0 = cq1;
+                double acc = -r67.x * u0;
+                acc = fma(r01.x * vj, (pq1 + mq1) - 2.0 * u0, acc);
+                acc = fma(g4h, pq1 - mq1, acc);
+                acc = fma(v01.y, (cq2 + cq0) - 2.0 * u0, acc);
+                acc = fma(v23.x, cq2 - cq0, acc);
+                acc = fma(r45.y * v23.y, (pq2 - pq0) - mqx, acc);
+                return yterm(full, u0, acc, r67.y, ed);
+            };
+            auto row = [&](int r, double& l, double& d, double& u) {
+                const int i = a + r;
+                double2 r01, r23, r45, r67;
+                rtab(i, r01, r23, r45, r67);
+                const double g4h = g4(r01, r23, r45);
+                if (r == 0) {
+                    if (a == 0) {
+                        // face plane i = 0 (discretization.cpp:318-329): one-sided g4 term, no cross
+                        cp_async_wait<kRing - 1>();  // row 2 (ring slot 0)
+                        const double n0 = *slot(0, 0), n1 = *slot(0, 1), n2 = *slot(0, 2);
+                        const double u0 = c1;
+                        double acc = -r67.x * u0;
+                        acc = fma(g4h, order2r ? fma(4.0, p1, -n1) - 3.0 * u0 : 2.0 * (p1 - u0), acc);
+                        acc = fma(v01.y, (c2 + c0) - 2.0 * u0, acc);
+                        acc = fma(v23.x, c2 - c0, acc);
+                        double x0 = yterm(false, u0, acc, r67.y, ce);
+                        // r_min Dirichlet ranks below r_max / y_max / v_max (discretization.cpp:153-192)
+                        if (rminD && !(kN && ymaxD)) x0 = rminv - u0;
+                        x[0] = x0;
+                        // the super2 fold needs row 1's rhs (solver.cpp:28-40)
+                        double2 q01, q23, q45, q67;
+                        rtab(1, q01, q23, q45, q67);
+                        const double g4h1 = g4(q01, q23, q45);
+                        const double x1 = stencil(false, q01, q45, q67, g4h1, c2 - c0, c1, p0, p1, p2, n0, n1, n2, pe);
+                        double d0, u0c, s20, l1, d1, u1, t1, l0;
+                        coeffs(0, r01.x * vj, g4h, l0, d0, u0c, s20);
+                        double f0d = d0, f0u = u0c;
+                        if (s20 != 0.0) {
+                            coeffs(1, q01.x * vj, g4h1, l1, d1, u1, t1);
+                            if (fabs(u1) > 1e-300) {
+                                const double f = s20 / u1;
+                                f0d = fma(-f, l1, d0);
+                                f0u = fma(-f, d1, u0c);
+                                x[0] = fma(-f, x1, x[0]);
+                            } else {  // lagged fold: row 2's rhs (rows 1..3 of the window)
+                                cp_async_wait<kRing - 2>();
+                                double2 w01, w23, w45, w67;
+                                rtab(2, w01, w23, w45, w67);
+                                const double x2 = stencil(false, w01, w45, w67, g4(w01, w23, w45), p2 - p0, p1, n0,
+                                                          n1, n2, *slot(1, 0), *slot(1, 1), *slot(1, 2),
+                                                          edge ? *slot(0, 3) : 0.0);
+                                x[0] = fma(-s20, x2, x[0]);
+                            }
+                        }
+                        l = 0.0; d = f0d; u = f0u;
+                        return;
+                    }
+                    x[0] = stencil(false, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
+                } else {
+                    shift(r);
+                    const double xv = stencil(true, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
+                    // face plane i = nr-1: r_max is always Dirichlet and ranks first
+                    x[r] = (r == M - 1 && i == nr - 1 && rmaxD) ? rmaxv - c1 : xv;
+                }
+                // rows a+1 .. a+14 are always interior; a+15 may be the r_max face
+                if (r == M - 1 && i == nr - 1 && rmaxD) {
+                    l = 0.0; d = 1.0; u = 0.0;
+                } else {
+                    interior(r01.x * vj, g4h, l, d, u);
+                }
+            };
+            ok = seg_solve<M>(M, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
+            cp_async_wait<0>();
+            // STAGE: queue the next tile's window and ring rows now (the ring and
+            // the window registers are free), ahead of this tile's reduced systems
+            if constexpr (STAGE) {
+                if (t + 1 < TPC) {
+                    const int kn = tile_k(t + 1);
+                    const bool ed = tx == 0 || (tx == KL - 1 && kn != NY - 1);
+                    prologue_staged(jd, v.U + off + static_cast<size_t>(j) * NY + kn, ed, tx == 0 ? -1 : 1);
+                }
+            }
         };
-        // y-direction terms and the k faces (discretization.cpp:340-352)
-        // full: every lane of the warp is here (rows r >= 1); row 0 runs the
-        // face-row code in half-warp 0 of warp 0 only, so it shuffles per half-warp
-        auto yterm = [&](bool full, double u0, double acc, double a_i, double ed) {
-            const unsigned msk = full ? 0xffffffffu : hmask;
-            double kl = __shfl_up_sync(msk, u0, 1, 16);
-            double kr = __shfl_down_sync(msk, u0, 1, 16);
-            if (tx == 0 && !k0) kl = ed;
-            if (tx == 15 && !kN) kr = ed;
-            double yd = kr - kl;
-            if (k0)  // one-sided y row (discretization.cpp:346-352); ed = U(i, j, 2)
-                yd = order2y ? fma(4.0, kr, -ed) - 3.0 * u0 : 2.0 * (kr - u0);
-            acc = fma(fma(a_i, vs6, t6), yd, acc);
-            return acc * dtm;  // y-face Dirichlet columns are fixed up after the march
-        };
-        // dU0 at an interior row i from a window (mm, cc, pp)
-        auto stencil = [&](bool full, const double2& r01, const double2& r45, const double2& r67,
-                           double g4h, double mqx, double mq1, double cq0, double cq1,
-                           double cq2, double pq0, double pq1, double pq2, double ed) {
-            const double u0 = cq1;
-            double acc = -r67.x * u0;
-            acc = fma(r01.x * vj, (pq1 + mq1) - 2.0 * u0, acc);
-            acc = fma(g4h, pq1 - mq1, acc);
-            acc = fma(v01.y, (cq2 + cq0) - 2.0 * u0, acc);
-            acc = fma(v23.x, cq2 - cq0, acc);
-            acc = fma(r45.y * v23.y, (pq2 - pq0) - mqx, acc);
-            return yterm(full, u0, acc, r67.y, ed);
-        };
-        auto row = [&](int r, double& l, double& d, double& u) {
-            const int i = a + r;
-            double2 r01, r23, r45, r67;
-            rtab(i, r01, r23, r45, r67);
-            const double g4h = g4(r01, r23, r45);
-            if (r == 0) {
-                if (a == 0) {
-                    // face plane i = 0 (discretization.cpp:318-329): one-sided g4 term, no cross
-                    cp_async_wait<kRing - 1>();  // row 2 (ring slot 0)
-                    const double n0 = *slot(0, 0), n1 = *slot(0, 1), n2 = *slot(0, 2);
-                    const double u0 = c1;
-                    double acc = -r67.x * u0;
-                    acc = fma(g4h, order2r ? fma(4.0, p1, -n1) - 3.0 * u0 : 2.0 * (p1 - u0), acc);
-                    acc = fma(v01.y, (c2 + c0) - 2.0 * u0, acc);
-                    acc = fma(v23.x, c2 - c0, acc);
-                    double x0 = yterm(false, u0, acc, r67.y, ce);
-                    // r_min Dirichlet ranks below r_max / y_max / v_max (discretization.cpp:153-192)
-                    if (rminD && !(kN && ymaxD)) x0 = rminv - u0;
-                    x[0] = x0;
-                    // the super2 fold needs row 1's rhs (solver.cpp:28-40)
-                    double2 q01, q23, q45, q67;
-                    rtab(1, q01, q23, q45, q67);
-                    const double g4h1 = g4(q01, q23, q45);
-                    const double x1 = stencil(false, q01, q45, q67, g4h1, c2 - c0, c1, p0, p1, p2, n0, n1, n2, pe);
-                    double d0, u0c, s20, l1, d1, u1, t1, l0;
-                    coeffs(0, r01.x * vj, g4h, l0, d0, u0c, s20);
-                    double f0d = d0, f0u = u0c;
-                    if (s20 != 0.0) {
-                        coeffs(1, q01.x * vj, g4h1, l1, d1, u1, t1);
-                        if (fabs(u1) > 1e-300) {
-                            const double f = s20 / u1;
-                            f0d = fma(-f, l1, d0);
-                            f0u = fma(-f, d1, u0c);
-                            x[0] = fma(-f, x1, x[0]);
-                        } else {  // lagged fold: row 2's rhs (rows 1..3 of the window)
-                            cp_async_wait<kRing - 2>();
-                            double2 w01, w23, w45, w67;
-                            rtab(2, w01, w23, w45, w67);
-                            const double x2 = stencil(false, w01, w45, w67, g4(w01, w23, w45), p2 - p0, p1, n0,
-                                                      n1, n2, *slot(1, 0), *slot(1, 1), *slot(1, 2),
-                                                      edge ? *slot(0, 3) : 0.0);
-                            x[0] = fma(-s20, x2, x[0]);
+        if (jdeg) march(std::true_type{});
+        else march(std::false_type{});
+        if (!ok) record_pivot(st, s, 0, j * NY + k, a + bad_r);
+        // reduced-system rows as [column][field][segment] (field stride S+1, column
+        // stride 8S+9: conflict-free for the writers, lanes = k, and for the
+        // scans, lanes = segments)
+        double* E = red + tx * CST + sg;
+        E[0] = yF; E[FS] = aF; E[2 * FS] = bF; E[3 * FS] = yL; E[4 * FS] = aL; E[5 * FS] = bL;
+        __syncthreads();
+        if (S > 1) {
+            if constexpr (SCAN) {
+                // every thread solves: column tid / S, segment tid % S (KL S threads)
+                const int cc = tid / S, ts = tid - cc * S;
+                double* Ec = red + cc * CST + ts;
+                const int kk = (kt0 + t) * KL + cc;
+                const bool csolve = !(kk == NY - 1 && ymaxD) && !(j == NV - 1 && dir(v, F_VMAX)) &&
+                                    !(kk == 0 && yminD) && !(j == 0 && dir(v, F_VMIN));
+                const double eyF = Ec[0], eaF = Ec[FS], ebF = Ec[2 * FS], eyL = Ec[3 * FS], eaL = Ec[4 * FS],
+                             ebL = Ec[5 * FS];
+                double lf = 0.0, rg = 0.0;
+                int bad = 0;
+                if (S == 16) bad = reduced_scan<16>(eyF, eaF, ebF, eyL, eaL, ebL, ts, S, lf, rg);
+                else bad = reduced_scan<32>(eyF, eaF, ebF, eyL, eaL, ebL, ts, S, lf, rg);
+                if (v.dbg & 1) lf = rg = 0.0;  // diagnostic: uncoupled segments (wrong results, finite)
+                if (csolve && bad) record_pivot(st, s, 0, j * NY + kk, bad * M);
+                Ec[6 * FS] = lf;  // x_{a-1} of segment ts
+                Ec[7 * FS] = rg;  // x_{a+m} of segment ts
+            } else if (KL == 16 && sg < 2) {  // warp 0: segment rows 0 (forward) and 1 (backward) of every column
+                const unsigned mask = __ballot_sync(0xffffffffu, solve);
+                if (solve) {
+                    int bt = 0;
+                    if (!reduced_solve_2way(red + tx * CST, S, 1, FS, sg == 1, mask, 16, bt))
+                        record_pivot(st, s, 0, j * NY + k, bt * M);
+                    __syncwarp(mask);
+                    // p_t, q_t -> each segment's left (p_{t-1}) / right (q_t), as the scan leaves them
+                    if (sg == 0) {
+                        for (int ts = S - 1; ts >= 0; --ts) {
+                            double* et = red + tx * CST + ts;
+                            et[6 * FS] = ts > 0 ? et[-1 + 6 * FS] : 0.0;
                         }
                     }
-                    l = 0.0; d = f0d; u = f0u;
-                    return;
-                }
-                x[0] = stencil(false, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
-            } else {
-                shift(r);
-                const double xv = stencil(true, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
-                // face plane i = nr-1: r_max is always Dirichlet and ranks first
-                x[r] = (r == M - 1 && i == nr - 1 && rmaxD) ? rmaxv - c1 : xv;
-            }
-            // rows a+1 .. a+14 are always interior; a+15 may be the r_max face
-            if (r == M - 1 && i == nr - 1 && rmaxD) {
-                l = 0.0; d = 1.0; u = 0.0;
-            } else {
-                interior(r01.x * vj, g4h, l, d, u);
-            }
-        };
-        ok = seg_solve<M>(M, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
-        cp_async_wait<0>();
-    };
-    if (jdeg) march(std::true_type{});
-    else march(std::false_type{});
-    if (!ok) record_pivot(st, s, 0, j * NY + k, a + bad_r);
-    // reduced-system rows as [column][field][segment] (field stride S+1, column
-    // stride 8S+9: conflict-free for the writers, lanes = k, and for the
-    // scans, lanes = segments)
-    const int FS = S + 1, CST = 8 * S + 9;
-    double* E = red + tx * CST + sg;
-    E[0] = yF; E[FS] = aF; E[2 * FS] = bF; E[3 * FS] = yL; E[4 * FS] = aL; E[5 * FS] = bL;
-    __syncthreads();
-    if (S > 1) {
-        if constexpr (SCAN) {
-            // every thread solves: column tid / S, segment tid % S (16 S threads)
-            const int cc = tid / S, t = tid - cc * S;
-            double* Ec = red + cc * CST + t;
-            const int kk = (blockIdx.x - j * TK) * 16 + cc;
-            const bool csolve = !(kk == NY - 1 && ymaxD) && !(j == NV - 1 && dir(v, F_VMAX)) &&
-                                !(kk == 0 && yminD) && !(j == 0 && dir(v, F_VMIN));
-            const double eyF = Ec[0], eaF = Ec[FS], ebF = Ec[2 * FS], eyL = Ec[3 * FS], eaL = Ec[4 * FS],
-                         ebL = Ec[5 * FS];
-            double lf = 0.0, rg = 0.0;
-            int bad = 0;
-            if (S == 16) bad = reduced_scan<16>(eyF, eaF, ebF, eyL, eaL, ebL, t, S, lf, rg);
-            else bad = reduced_scan<32>(eyF, eaF, ebF, eyL, eaL, ebL, t, S, lf, rg);
-            if (v.dbg & 1) lf = rg = 0.0;  // diagnostic: uncoupled segments (wrong results, finite)
-            if (csolve && bad) record_pivot(st, s, 0, j * NY + kk, bad * M);
-            Ec[6 * FS] = lf;  // x_{a-1} of segment t
-            Ec[7 * FS] = rg;  // x_{a+m} of segment t
-        } else if (sg < 2) {  // warp 0: segment rows 0 (forward) and 1 (backward) of every column
-            const unsigned mask = __ballot_sync(0xffffffffu, solve);
-            if (solve) {
-                int bt = 0;
-                if (!reduced_solve_2way(red + tx * CST, S, 1, FS, sg == 1, mask, 16, bt))
-                    record_pivot(st, s, 0, j * NY + k, bt * M);
-                __syncwarp(mask);
-                // p_t, q_t -> each segment's left (p_{t-1}) / right (q_t), as the scan leaves them
-                if (sg == 0) {
-                    for (int t = S - 1; t >= 0; --t) {
-                        double* et = red + tx * CST + t;
-                        et[6 * FS] = t > 0 ? et[-1 + 6 * FS] : 0.0;
-                    }
                 }
             }
         }
-    }
-    __syncthreads();
-    const double left = (solve && sg > 0) ? E[6 * FS] : 0.0;        // x_{a-1}
-    const double right = (solve && sg < S - 1) ? E[7 * FS] : 0.0;   // x_{a+m}
-    if (kface) {
-        // y_max / y_min Dirichlet columns (identity rows): dU0 = face(t_next) - U
-        // (solver.cpp:111-116) wherever the r faces do not take precedence
-        // (discretization.cpp:153-192: r_max > y_max > v_max > r_min > y_min > v_min)
+        __syncthreads();
+        const double left = (solve && sg > 0) ? E[6 * FS] : 0.0;        // x_{a-1}
+        const double right = (solve && sg < S - 1) ? E[7 * FS] : 0.0;   // x_{a+m}
+        if (kface) {
+            // y_max / y_min Dirichlet columns (identity rows): dU0 = face(t_next) - U
+            // (solver.cpp:111-116) wherever the r faces do not take precedence
+            // (discretization.cpp:153-192: r_max > y_max > v_max > r_min > y_min > v_min)
 #pragma unroll
-        for (int r = 0; r < M; ++r) {
-            const int i = a + r;
-            if (!((i == nr - 1 && rmaxD) || (i == 0 && rminD && !(kN && ymaxD))))
-                x[r] = fyk[i] - __ldg(col + static_cast<size_t>(i) * SR);
+            for (int r = 0; r < M; ++r) {
+                const int i = a + r;
+                if (!((i == nr - 1 && rmaxD) || (i == 0 && rminD && !(kN && ymaxD))))
+                    x[r] = fyk[i] - __ldg(col + static_cast<size_t>(i) * SR);
+            }
         }
-    }
-    double b = bL;
-    double* __restrict__ dcol = v.D + off + static_cast<size_t>(j) * NY + k + static_cast<size_t>(a) * SR;
+        double b = bL;
+        double* __restrict__ dcol = v.D + off + static_cast<size_t>(j) * NY + k + static_cast<size_t>(a) * SR;
 #pragma unroll
-    for (int r = M - 1; r >= 0; --r) {
-        if (r < M - 1) b = -cs[r] * b;
-        dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(al[r], left, x[r]));
+        for (int r = M - 1; r >= 0; --r) {
+            if (r < M - 1) b = -cs[r] * b;
+            dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(al[r], left, x[r]));
+        }
+        if (TPC > 1 && t + 1 < TPC) __syncthreads();  // the reduced rows are reused by the next tile
     }
     tl_end(v, s, 0);
 }
 
-inline size_t pa_smem(int nr) {
-    const int S = nr / 16, nt = 16 * S;
-    return sizeof(double) * (static_cast<size_t>(16) * (8 * S + 9) + static_cast<size_t>(kRing * 4 + 1) * nt +
+inline size_t pa_smem(int nr, int kl = 16, int tpc = 1) {
+    const int S = nr / 16, nt = kl * S;
+    const int rst = kRing * 4 + (tpc > 1 ? 12 : 0) + 1;
+    return sizeof(double) * (static_cast<size_t>(kl) * (8 * S + 9) + static_cast<size_t>(rst) * nt +
                              static_cast<size_t>(nr) * (kFR + 2));
 }
 
@@ -2435,8 +2526,29 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
     if (pa) {
         // pass A fused: explicit stencil + r-lines
         const int S = v.nr / 16;
-        const dim3 g(v.nv * (v.ny / 16), v.P), b(16, S);
-        const size_t sm = pa_smem(v.nr);
+        // k-lane group width: 8 for 512-row lines (two 256-thread CTAs per SM
+        // instead of one 512-thread CTA), 16 otherwise; HJMSV_PA_KL overrides
+        static const int kl_env = [] {
+            const char* e = std::getenv("HJMSV_PA_KL");
+            return e ? std::atoi(e) : 0;
+        }();
+        const int KLw = (kl_env == 8 || kl_env == 16) ? kl_env : (S == 32 ? 16 : 16);
+        const bool kl8 = KLw == 8 && S >= 16 && (S & (S - 1)) == 0 && !(v.dbg & 2) && v.ny % 8 == 0;
+        const int KLu = kl8 ? 8 : 16;
+        // column tiles per CTA (HJMSV_PA_TPC = 1 or 2)
+        static const int tpc_env = [] {
+            const char* e = std::getenv("HJMSV_PA_TPC");
+            return e ? std::atoi(e) : 1;
+        }();
+        const int tpc = (tpc_env == 2 && !kl8 && (v.ny / KLu) % 2 == 0) ? 2 : 1;
+        const dim3 g(v.nv * (v.ny / KLu) / tpc, v.P), b(KLu, S);
+        // HJMSV_PA_PAD (diagnostic): extra dynamic shared memory per CTA, to pin
+        // fewer CTAs per SM in occupancy experiments
+        static const size_t pad_env = [] {
+            const char* e = std::getenv("HJMSV_PA_PAD");
+            return e ? static_cast<size_t>(std::atoll(e)) : size_t(0);
+        }();
+        const size_t sm = pa_smem(v.nr, KLu, tpc) + pad_env;
         // reduced systems of 16+ segments (nr >= 256) by lane scans over all
         // warps; shorter ones by warp 0's two-ended recurrence (measured faster:
         // the scan's registers make the march spill)
@@ -2445,17 +2557,34 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
             smem_attr(reinterpret_cast<const void*>(kern), sm);
             launch_pdl(kern, g, b, sm, stream, v, s);
         };
-        switch (shape) {
-            case 32: go(k_pa<32, 32, false>); break;
-            case 64: go(k_pa<64, 64, false>); break;
-            case 128:
-                if (scan) go(k_pa<128, 128, true>);
-                else go(k_pa<128, 128, false>);
-                break;
-            default:
-                if (scan) go(k_pa<256, 256, true>);
-                else go(k_pa<256, 256, false>);
-                break;
+        if (tpc == 2) {
+            switch (shape) {
+                case 32: go(k_pa<32, 32, false, 16, 2>); break;
+                case 64: go(k_pa<64, 64, false, 16, 2>); break;
+                case 128:
+                    if (scan) go(k_pa<128, 128, true, 16, 2>);
+                    else go(k_pa<128, 128, false, 16, 2>);
+                    break;
+                default:
+                    if (scan) go(k_pa<256, 256, true, 16, 2>);
+                    else go(k_pa<256, 256, false, 16, 2>);
+                    break;
+            }
+        } else {
+            switch (shape) {
+                case 32: go(k_pa<32, 32, false>); break;
+                case 64: go(k_pa<64, 64, false>); break;
+                case 128:
+                    if (kl8) go(k_pa<128, 128, true, 8>);
+                    else if (scan) go(k_pa<128, 128, true>);
+                    else go(k_pa<128, 128, false>);
+                    break;
+                default:
+                    if (kl8) go(k_pa<256, 256, true, 8>);
+                    else if (scan) go(k_pa<256, 256, true>);
+                    else go(k_pa<256, 256, false>);
+                    break;
+            }
         }
         mark(0, "fx_explicit_sweep_r", 16.0);
     } else {
@@ -2479,8 +2608,10 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         else if (shape == 64) launch_plane<64, 64, 1, 256>(v, s, stream);
         else if (shape == 128) {
             if (pl == 3) launch_plane<128, 128, 2, 256>(v, s, stream);  // cluster variant (diagnostic)
+            else if (pl == 4) launch_plane<128, 128, 1, 512>(v, s, stream);  // 16 warps (diagnostic)
             else launch_plane<128, 128, 1, 256>(v, s, stream);
-        } else launch_plane<256, 256, 4, 256>(v, s, stream);
+        } else if (pl == 4) launch_plane<256, 256, 4, 512>(v, s, stream);
+        else launch_plane<256, 256, 4, 256>(v, s, stream);
         mark(2, "fx_plane_vy_update", 24.0);
         return;
     }
