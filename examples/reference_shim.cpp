@@ -61,9 +61,13 @@ std::pair<Grid3, SolveReport> run_b200(const PdeProblem& pb, const SolverConfig&
     p.r = to_c(pb.r_axis);
     p.v = to_c(pb.v_axis);
     p.y = to_c(pb.y_axis);
-    // constant model functions only (ModelParams::constants, model.cpp:12-23)
-    p.model = {pb.model.kappa, pb.model.lambda_fn(0.0), pb.model.gamma_fn(0.0),
-               pb.model.eps_fn(0.0), pb.model.theta, pb.model.rho};
+    // ModelParams: the reference's TimeFn objects cross the C ABI as callbacks
+    // (fn_user = the ModelParams; called while the problem is lowered)
+    p.model = {pb.model.kappa, 0.0, 0.0, 0.0, pb.model.theta, pb.model.rho,
+               [](double t, void* u) { return static_cast<const ModelParams*>(u)->lambda_fn(t); },
+               [](double t, void* u) { return static_cast<const ModelParams*>(u)->gamma_fn(t); },
+               [](double t, void* u) { return static_cast<const ModelParams*>(u)->eps_fn(t); },
+               const_cast<ModelParams*>(&pb.model)};
     std::vector<double> T, D;
     for (auto& q : quotes) {
         T.push_back(q.first);
@@ -130,19 +134,27 @@ int main() {
     }
     const double base = 1.04, r0 = 0.01;
     const InitialCurve curve = InitialCurve::flat(base);
-    const ModelParams model = ModelParams::constants(0.05, 0.15, 0.9, 0.4, 1.2, -0.3);
+    const ModelParams model_const = ModelParams::constants(0.05, 0.15, 0.9, 0.4, 1.2, -0.3);
+    // time-dependent model functions (ModelParams::lambda_fn / gamma_fn / eps_fn)
+    ModelParams model_t = model_const;
+    model_t.lambda_fn = [](double t) { return 0.15 * (1.0 + 0.3 * std::sin(2.0 * t)); };
+    model_t.gamma_fn = [](double t) { return 0.9 - 0.05 * (1.0 - std::cos(t)); };
+    model_t.eps_fn = [](double t) { return 0.4 * std::exp(-0.1 * t); };
     SolverConfig cfg;  // reference defaults (solver.hpp:10-20)
     cfg.steps_per_year = 24;
     struct Case {
         const char* name;
         B200Instrument ins;
+        bool timefn;
     };
     const Case cases[] = {
-        {"zcb", {HJMSV_INSTRUMENT_ZCB, 5.0, 0.0, 0.0}},
-        {"caplet", {HJMSV_INSTRUMENT_CAPLET, 3.0, 3.25, 0.035}},
+        {"zcb", {HJMSV_INSTRUMENT_ZCB, 5.0, 0.0, 0.0}, false},
+        {"caplet", {HJMSV_INSTRUMENT_CAPLET, 3.0, 3.25, 0.035}, false},
+        {"caplet_timefn", {HJMSV_INSTRUMENT_CAPLET, 3.0, 3.25, 0.035}, true},
     };
     int bad = 0;
     for (const Case& cs : cases) {
+        const ModelParams& model = cs.timefn ? model_t : model_const;
         PdeProblem pb;
         pb.r_axis = uniform_axis(0.0, 25.0, 48);
         pb.v_axis = uniform_axis(0.0, 1.5, 24);

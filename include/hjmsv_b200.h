@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define HJMSV_ABI_VERSION 1
+#define HJMSV_ABI_VERSION 2
 
 /* Status codes. The C++ wrapper maps them back to the reference exception
  * types: INVALID_ARGUMENT -> std::invalid_argument, SINGULAR_PIVOT/NONFINITE/
@@ -64,9 +64,23 @@ typedef struct {
     double c1, c2;
 } hjmsv_axis;
 
-/* ModelParams::constants(kappa, lambda, gamma, eps, theta, rho) (model.cpp:12-23) */
+/* TimeFn (model.hpp:10): a deterministic model function of calendar time t.
+ * `user` is hjmsv_model::fn_user. Called on the host only, while a problem is
+ * lowered (hjmsv_solver_create / the stage entry points), possibly from several
+ * host threads at once for a batch. */
+typedef double (*hjmsv_time_fn)(double t, void* user);
+
+/* ModelParams (model.hpp:20-37). With every *_fn NULL this is
+ * ModelParams::constants(kappa, lambda, gamma, eps, theta, rho) (model.cpp:12-23).
+ * A non-NULL lambda_fn / gamma_fn / eps_fn replaces that constant by a function
+ * of t: HjmCoefficientField::prepare (discretization.cpp:40-54) evaluates them
+ * at every step's half level t_mid (solver.cpp:96), and so does the lowering,
+ * which then uploads per-step coefficient tables. ModelParams::validate checks
+ * gamma_fn(0) in (0,1] (model.cpp:36-37). */
 typedef struct {
     double kappa, lambda, gamma, eps, theta, rho;
+    hjmsv_time_fn lambda_fn, gamma_fn, eps_fn;
+    void* fn_user;
 } hjmsv_model;
 
 /* InitialCurve (curve.hpp): flat(base) (curve.cpp:11-20) or natural cubic

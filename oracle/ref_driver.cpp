@@ -92,7 +92,22 @@ InitialCurve to_curve(const hjmsv_curve& c) {
 }
 
 ModelParams to_model(const hjmsv_model& m) {
-    return ModelParams::constants(m.kappa, m.lambda, m.gamma, m.eps, m.theta, m.rho);
+    if (!m.lambda_fn && !m.gamma_fn && !m.eps_fn)
+        return ModelParams::constants(m.kappa, m.lambda, m.gamma, m.eps, m.theta, m.rho);
+    // model functions of t (ModelParams::lambda_fn / gamma_fn / eps_fn, model.hpp:22-24)
+    ModelParams p;
+    p.kappa = m.kappa;
+    p.theta = m.theta;
+    p.rho = m.rho;
+    auto fn = [&](hjmsv_time_fn f, double c) -> TimeFn {
+        if (f) return [f, u = m.fn_user](double t) { return f(t, u); };
+        return [c](double) { return c; };
+    };
+    p.lambda_fn = fn(m.lambda_fn, m.lambda);
+    p.gamma_fn = fn(m.gamma_fn, m.gamma);
+    p.eps_fn = fn(m.eps_fn, m.eps);
+    p.validate();
+    return p;
 }
 
 CapletSpec to_caplet(const hjmsv_problem& p) {

@@ -34,9 +34,14 @@ class CAxis(ctypes.Structure):
                 ("c1", c_double), ("c2", c_double)]
 
 
+# hjmsv_time_fn: double (*)(double t, void* user) — TimeFn (model.hpp:10)
+TIME_FN = ctypes.CFUNCTYPE(c_double, c_double, ctypes.c_void_p)
+
+
 class CModel(ctypes.Structure):
     _fields_ = [("kappa", c_double), ("lam", c_double), ("gamma", c_double), ("eps", c_double),
-                ("theta", c_double), ("rho", c_double)]
+                ("theta", c_double), ("rho", c_double), ("lambda_fn", TIME_FN), ("gamma_fn", TIME_FN),
+                ("eps_fn", TIME_FN), ("fn_user", ctypes.c_void_p)]
 
 
 class CCurve(ctypes.Structure):

@@ -233,6 +233,7 @@ struct hjmsv_solver {
     // device
     double *U = nullptr, *D = nullptr, *C = nullptr, *U0 = nullptr;
     double *axes = nullptr, *steps = nullptr, *fast = nullptr, *fb = nullptr;
+    double* ab = nullptr;      // per-step a_i, b_i (model functions of t only)
     ProblemConst* pc = nullptr;
     DevStatus* st = nullptr;
     long long* spot_idx = nullptr;
@@ -255,7 +256,7 @@ struct hjmsv_solver {
         if (stream) cudaStreamSynchronize(stream);  // buffers return to the pool only when idle
         if (graph) cudaGraphExecDestroy(graph);
         for (void* p : {(void*)U, (void*)D, (void*)C, (void*)U0, (void*)axes, (void*)steps,
-                        (void*)fast, (void*)fb, (void*)pc, (void*)st, (void*)spot_idx, (void*)spot_w,
+                        (void*)fast, (void*)fb, (void*)ab, (void*)pc, (void*)st, (void*)spot_idx, (void*)spot_w,
                         (void*)spot_out})
             dfree(p);
         if (ev0) cudaEventDestroy(ev0);
@@ -400,11 +401,22 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
             L[p].pc.dt = ov->dt_mult;
             L[p].pc.theta_dt = cfg.theta_cn * ov->dt;
             build_step_table(L[p], {ov->t_from}, ov->dt, ov->faces);
+            build_model_steps(L[p]);
         }
         if (L[p].nr != L[0].nr || L[p].nv != L[0].nv || L[p].ny != L[0].ny ||
             L[p].n_steps != L[0].n_steps)
             throw std::invalid_argument("batched problems must share grid dims and step count");
     }
+    // model functions of t anywhere in the batch: every problem gets per-step
+    // coefficient tables (a constant model's are its constants, step by step)
+    bool timedep = false;
+    for (int p = 0; p < count; ++p) timedep = timedep || L[p].timedep;
+    if (timedep)
+        for (int p = 0; p < count; ++p)
+            if (!L[p].timedep) {
+                L[p].timedep = true;
+                build_model_steps(L[p]);
+            }
     if (mode == HJMSV_MODE_FAST && !fast_supported(L[0].nr, L[0].nv, L[0].ny))
         throw Failure(HJMSV_UNSUPPORTED, "FAST kernels do not support this grid shape");
     int ndev = 0;
@@ -473,6 +485,13 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
             h->term_steps[p].push_back(l.steps[static_cast<size_t>(s) * kStepStride + ST_TNEXT]);
     }
     CK(cudaMemcpyAsync(h->axes, axes_h, sizeof(double) * axes_n, cudaMemcpyHostToDevice, h->stream));
+    if (timedep) {  // [P][S][2 nr] a_i, b_i of every step's prepare(t_mid)
+        const size_t ab_n = 2 * static_cast<size_t>(h->nr) * h->S;
+        h->ab = dalloc<double>(static_cast<size_t>(count) * ab_n);
+        for (int p = 0; p < count; ++p)
+            CK(cudaMemcpy(h->ab + static_cast<size_t>(p) * ab_n, L[p].ab_steps.data(), sizeof(double) * ab_n,
+                          cudaMemcpyHostToDevice));
+    }
     CK(cudaMemcpyAsync(h->steps, steps_h, sizeof(double) * steps_n, cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));  // the staging buffer is released with this scope
     CK(cudaMemcpy(h->pc, pcs.data(), sizeof(ProblemConst) * count, cudaMemcpyHostToDevice));
@@ -500,6 +519,8 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
     v.axes_stride = astride;
     v.pc = h->pc;
     v.steps = h->steps;
+    v.ab = h->ab;
+    v.fast_step = 0;
     v.st = h->st;
     v.apply_only = ov && ov->apply_only ? 1 : 0;
     v.dmask = 0;
@@ -515,7 +536,11 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
     }
     h->stage = ov != nullptr;
     if (mode == HJMSV_MODE_FAST) {
-        v.fast_stride = fast_stride(h->nr, h->nv, h->ny);
+        // one table per problem, or one per (problem, step) with model functions of t
+        const int tab = fast_stride(h->nr, h->nv, h->ny);
+        const int nsteps_tab = timedep ? h->S : 1;
+        v.fast_step = timedep ? tab : 0;
+        v.fast_stride = tab * nsteps_tab;
         h->fast = dalloc<double>(static_cast<size_t>(count) * v.fast_stride);
         v.fast = h->fast;
         v.fb_stride = 2 * h->ny + 2 * h->nr + 2 * h->nr * h->ny;
@@ -525,8 +550,11 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         PinnedLease fstage(sizeof(double) * fast_n);
         double* fast_h = fstage.as<double>();
         parallel_for(count, count >= 64 ? host_workers() : 1, [&](int p) {
-            const std::vector<double> ft = build_fast_tables(L[p], cfg, L[p].pc.theta_dt);
-            std::copy(ft.begin(), ft.end(), fast_h + static_cast<size_t>(p) * v.fast_stride);
+            for (int st = 0; st < nsteps_tab; ++st) {
+                const std::vector<double> ft = build_fast_tables(L[p], cfg, L[p].pc.theta_dt, timedep ? st : -1);
+                std::copy(ft.begin(), ft.end(),
+                          fast_h + static_cast<size_t>(p) * v.fast_stride + static_cast<size_t>(st) * tab);
+            }
         });
         CK(cudaMemcpyAsync(h->fast, fast_h, sizeof(double) * fast_n, cudaMemcpyHostToDevice, h->stream));
         CK(cudaStreamSynchronize(h->stream));
@@ -552,6 +580,8 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         l.init.shrink_to_fit();
         l.steps.clear();
         l.steps.shrink_to_fit();
+        l.ab_steps.clear();
+        l.ab_steps.shrink_to_fit();
     }
     h->low = std::move(L);
     pt.mark("U0 -> U, status");
@@ -950,9 +980,6 @@ int32_t hjmsv_mc_price(const hjmsv_problem* problem, const hjmsv_mc_config* cfg,
         mp.theta = md.theta;
         mp.rho = md.rho;
         mp.sq1mr2 = std::sqrt(1.0 - md.rho * md.rho);
-        mp.lambda = md.lambda;
-        mp.gamma = md.gamma;
-        mp.eps = md.eps;
         mp.caplet = m.caplet;
         mp.accrual = m.accrual;
         mp.ratio = m.ratio;
@@ -961,10 +988,10 @@ int32_t hjmsv_mc_price(const hjmsv_problem* problem, const hjmsv_mc_config* cfg,
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         const long long want = (cfg->n_paths + 255) / 256;
         const int blocks = static_cast<int>(std::min<long long>(want, 8LL * sms));
-        double* f = dalloc<double>(m.f_next.size());
+        double* f = dalloc<double>(m.steps.size());
         double* part = dalloc<double>(2 * static_cast<size_t>(blocks));
         std::vector<double> ph(2 * static_cast<size_t>(blocks));
-        cudaError_t e = cudaMemcpy(f, m.f_next.data(), sizeof(double) * m.f_next.size(),
+        cudaError_t e = cudaMemcpy(f, m.steps.data(), sizeof(double) * m.steps.size(),
                                    cudaMemcpyHostToDevice);
         if (e == cudaSuccess) {
             mc_simulate(mp, f, part, blocks, nullptr);

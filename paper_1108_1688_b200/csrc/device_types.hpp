@@ -22,7 +22,8 @@ enum StepSlot : int {
     ST_TNEXT = 2,
     ST_TMID = 3,
     ST_RATIO = 4,   // [kMaxTerms]
-    ST_G = 16       // [kMaxTerms]
+    ST_G = 16,      // [kMaxTerms]
+    ST_HEPS2 = 28   // eps(t_mid)^2 / 2 (discretization.cpp:45)
 };
 
 // Face order = reference Face enum (discretization.hpp:84).
@@ -65,6 +66,10 @@ struct BatchView {
     DevStatus* st;        // [P]
     const double* fast;   // [P][fast_stride] derived factor tables (FAST mode)
     int fast_stride;
+    // time-dependent model functions (hjmsv_model::*_fn): the factor tables of
+    // step s start fast_step doubles after step 0's (0: one table for every step)
+    int fast_step;
+    const double* ab;     // [P][S][2 nr] a_i, b_i of prepare(t_mid) per step, or null (constant: axes block)
     int apply_only;       // stage mode: D = F(U), Dirichlet nodes 0 (apply_operator)
     int dmask;            // bit f set when face f is Dirichlet (uniform across the batch)
     double* fb;           // [P][fb_stride] Dirichlet face values at t_next of the current step
@@ -142,12 +147,13 @@ struct McParams {
     int full_truncation;
     unsigned long long seed;
     double dt, sqrt_dt, decay_y, decay_h, f0;
-    double kappa, theta, rho, sq1mr2, lambda, gamma, eps;
+    double kappa, theta, rho, sq1mr2;
     int caplet;
     double accrual, ratio, g;
 };
-// partial[2*b] = sum, partial[2*b+1] = sum of squares of block b's path samples
-void mc_simulate(const McParams& mp, const double* f_next, double* partial, int blocks,
+// partial[2*b] = sum, partial[2*b+1] = sum of squares of block b's path samples;
+// steps: per step (f(0, (s+1) dt), lambda, gamma, eps)
+void mc_simulate(const McParams& mp, const double* steps, double* partial, int blocks,
                  cudaStream_t stream);
 // extract_greeks of problem p's level (instruments.cpp:90-132); scale: rho /= r0
 // as finish() does (instruments.cpp:150-152). rho / vega may be null.

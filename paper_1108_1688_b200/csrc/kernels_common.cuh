@@ -13,9 +13,13 @@ namespace dev {
 
 struct Tab {
     const double *rz, *rj1, *rj2, *vz, *vj1, *vj2, *yz, *yj1, *yj2, *a, *b;
+    double heps2;  // eps(t_mid)^2 / 2 of the step (HjmCoefficientField::half_eps2_)
 };
 
-__device__ __forceinline__ Tab tables(const BatchView& v, int p) {
+// the axes of problem p and the a_i, b_i of prepare(t_mid) at step s
+// (discretization.cpp:40-54): the axes block for constant models, the per-step
+// block for time-dependent model functions
+__device__ __forceinline__ Tab tables(const BatchView& v, int p, int s) {
     const double* t = v.axes + static_cast<size_t>(p) * v.axes_stride;
     Tab x;
     x.rz = t;
@@ -30,8 +34,9 @@ __device__ __forceinline__ Tab tables(const BatchView& v, int p) {
     x.yj1 = t + v.ny;
     x.yj2 = t + 2 * v.ny;
     t += 3 * v.ny;
-    x.a = t;
-    x.b = t + v.nr;
+    x.a = v.ab ? v.ab + (static_cast<size_t>(p) * v.S + s) * 2 * v.nr : t;
+    x.b = x.a + v.nr;
+    x.heps2 = v.steps[(static_cast<size_t>(p) * v.S + s) * kStepStride + ST_HEPS2];
     return x;
 }
 

@@ -58,8 +58,8 @@ __device__ __forceinline__ double frcp(double x) {
 struct FT {
     const double *R, *V, *Y;
 };
-__device__ __forceinline__ FT ftab(const BatchView& v, int p) {
-    const double* t = v.fast + static_cast<size_t>(p) * v.fast_stride;
+__device__ __forceinline__ FT ftab(const BatchView& v, int p, int s) {
+    const double* t = v.fast + static_cast<size_t>(p) * v.fast_stride + static_cast<size_t>(s) * v.fast_step;
     FT f;
     f.R = t;
     f.V = t + kFR * v.nr;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) k_fx_explicit(BatchView v, int s) {
     const int q = (i * nv + j) * ny + k;
     const double* __restrict__ u = v.U + off + q;
     const double* step = step_row(v, p, s);
-    const FT F = ftab(v, p);
+    const FT F = ftab(v, p, s);
     const double* R = F.R + kFR * i;
     const double* V = F.V + kFV * j;
     const double* Y = F.Y + kFY * k;
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256) k_fx_explicit(BatchView v, int s) {
     } else {
         const int face = dface(v, i, j, k);
         if (face >= 0) {
-            out = v.apply_only ? 0.0 : face_value(pc, step, tables(v, p), face, i, k) - u[0];
+            out = v.apply_only ? 0.0 : face_value(pc, step, tables(v, p, s), face, i, k) - u[0];
         } else {
             const double vj = V[FV_V];
             const double g1s = R[FR_G1] * vj;
@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(512) k_fx_r(BatchView v, int s) {
     }
     double* E = red + (tx * S + sg) * 8;
     if (solve) {
-        const FT F = ftab(v, p);
+        const FT F = ftab(v, p, s);
         const double c4 = step_row(v, p, s)[ST_C4];
         const double vj = F.V[kFV * j + FV_V];
         const double yk = F.Y[kFY * k + FY_Y];
@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(512, 2) k_fx_v(BatchView v, int s) {
                        !(k == 0 && dir(v, F_YMIN));
     const int a = sg * kSegV;
     const int m = min(kSegV, nv - a);
-    const FT F = ftab(v, p);
+    const FT F = ftab(v, p, s);
     const double* T = F.V + kFV * a;
     double* __restrict__ col = v.D + static_cast<size_t>(p) * v.N +
                                (static_cast<size_t>(i) * nv + a) * ny + (k < ny ? k : 0);
@@ -896,7 +896,7 @@ __global__ void __launch_bounds__(256, 2) k_fx_y(BatchView v, int s) {
     double x[kSegY], cs[kSegY], al[kSegY];
 #pragma unroll
     for (int r = 0; r < kSegY; ++r) x[r] = r < m ? v.D[lb + r] : 0.0;
-    const FT F = ftab(v, p);
+    const FT F = ftab(v, p, s);
     double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
     if (solve && m > 0) {
         const double th = pc.theta_dt;
@@ -991,7 +991,7 @@ __global__ void __launch_bounds__(256, 2) k_fx_y(BatchView v, int s) {
                 md = bits > md ? bits : md;
             }
             const int face = dface(v, i, j, kk);
-            if (face >= 0) un = face_value(pc, step, tables(v, p), face, i, kk);
+            if (face >= 0) un = face_value(pc, step, tables(v, p, s), face, i, kk);
             Urow[r] = un;
             const unsigned long long flat = static_cast<unsigned long long>(lb - off + r);
             if (!isfinite(un)) {
@@ -1058,7 +1058,7 @@ __device__ __forceinline__ double face_entry(const BatchView& v, int p, int s, i
         k = t - i * ny;
     }
     if (!(v.dmask >> face & 1)) return 0.0;
-    return face_value(v.pc[p], step_row(v, p, s), tables(v, p), face, i, k);
+    return face_value(v.pc[p], step_row(v, p, s), tables(v, p, s), face, i, k);
 }
 
 __global__ void __launch_bounds__(256) k_faces(BatchView v, int s) {
@@ -1111,7 +1111,7 @@ __device__ __noinline__ double explicit_slow(const BatchView v, int p, int s, in
     const double* u = v.U + static_cast<size_t>(p) * v.N + (static_cast<size_t>(i) * nv + j) * ny + k;
     const int face = dface(v, i, j, k);
     if (face >= 0) return v.apply_only ? 0.0 : fval(v, p, face, i, k) - u[0];
-    const FT F = ftab(v, p);
+    const FT F = ftab(v, p, s);
     const double* R = F.R + kFR * i;
     const double* V = F.V + kFV * j;
     const double* Y = F.Y + kFY * k;
@@ -1193,7 +1193,7 @@ __global__ void __launch_bounds__(256) k_ex4(BatchView v, int s) {
     const double rp = __ldg(u + SR), rm = __ldg(u - SR);
     const double vp = __ldg(u + NY), vm = __ldg(u - NY);
     const double cross = (__ldg(u + SR + NY) - __ldg(u + SR - NY)) - (__ldg(u - SR + NY) - __ldg(u - SR - NY));
-    const FT F = ftab(v, p);
+    const FT F = ftab(v, p, s);
     const double2* R2 = reinterpret_cast<const double2*>(F.R + kFR * i);
     const double2 r01 = __ldg(R2), r23 = __ldg(R2 + 1), r45 = __ldg(R2 + 2), r67 = __ldg(R2 + 3);
     // r01 = (G1, G4C), r23 = (G4P, G4Q), r45 = (G4V, G3), r67 = (REACT, A)
@@ -1264,7 +1264,7 @@ __global__ void __launch_bounds__(256, 2) k_y3(BatchView v, int s) {
     double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
     if (solve) {
         const ProblemConst& pc = v.pc[p];
-        const FT F = ftab(v, p);
+        const FT F = ftab(v, p, s);
         const double th = pc.theta_dt;
         const double h1 = F.R[kFR * i + FR_A] * F.V[kFV * j + FV_V];
         const double react = F.R[kFR * i + FR_REACT];
@@ -1475,7 +1475,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const unsigned hmask = (KL == 16 ? 0xffffu : 0xffu) << ((sg & (32 / KL - 1)) * KL);
     const int a = sg * M;
     const size_t off = static_cast<size_t>(p) * v.N;
-    const FT F = ftab(v, p);
+    const FT F = ftab(v, p, s);
     // r-table and y-face values into shared memory by two bulk copies, overlapped
     // with the window prologue below
     __shared__ alignas(8) unsigned long long tbar;
@@ -1984,7 +1984,7 @@ k_plane(BatchView v, int s) {
     };
     const size_t off = static_cast<size_t>(p) * v.N;
     const size_t pb = off + (static_cast<size_t>(i) * NV + j0) * NY;  // first row of this CTA
-    const FT F = ftab(v, p);
+    const FT F = ftab(v, p, s);
     // per-plane scalars, loaded while the plane is staged
     const ProblemConst& pc = v.pc[p];
     const double th = pc.theta_dt, bound = pc.bound;
@@ -2365,7 +2365,7 @@ k_plane(BatchView v, int s) {
     if (v.fb_next && s + 1 < v.S) {
         double* fbn = v.fb_next + static_cast<size_t>(p) * v.fb_stride;
         const double* stp = step_row(v, p, s + 1);
-        const Tab T = tables(v, p);
+        const Tab T = tables(v, p, s);
         const bool rface = i == 0 || i == nr - 1;
         const int n_ent = (c == 0 ? 2 : 0) + 2 * (NY / CS) + (rface && c == 0 ? NY : 0);
         for (int e = tid; e < n_ent; e += NT) {

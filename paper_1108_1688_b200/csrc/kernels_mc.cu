@@ -39,7 +39,9 @@ __device__ __forceinline__ double u53(uint32_t a, uint32_t b) {
     return (static_cast<double>(m) + 0.5) * 0x1.0p-53;
 }
 
-__global__ void __launch_bounds__(256) k_mc(McParams mp, const double* __restrict__ f_next,
+// per step s: steps[4s..4s+3] = f(0, (s+1) dt), lambda(s dt), gamma(s dt), eps(s dt)
+// (the model functions at the step's start, montecarlo.cpp:55-58)
+__global__ void __launch_bounds__(256) k_mc(McParams mp, const double* __restrict__ steps,
                                             double* __restrict__ partial) {
     __shared__ double ssum[256], ssq[256];
     const long long tid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -50,9 +52,11 @@ __global__ void __launch_bounds__(256) k_mc(McParams mp, const double* __restric
         double x = 0.0, y = 0.0, v = 1.0, integral_r = 0.0;
         double r = mp.f0;
         for (int s = 0; s < mp.n_steps; ++s) {
+            const double2 fl = __ldg(reinterpret_cast<const double2*>(steps) + 2 * s);      // f_next, lambda
+            const double2 ge = __ldg(reinterpret_cast<const double2*>(steps) + 2 * s + 1);  // gamma, eps
             const double v_pos = mp.full_truncation ? fmax(v, 0.0) : fabs(v);
             const double r_pos = fmax(r, 0.0);
-            const double eta = sqrt(v_pos) * mp.lambda * (r_pos > 0.0 ? pow(r_pos, mp.gamma) : 0.0);
+            const double eta = sqrt(v_pos) * fl.y * (r_pos > 0.0 ? pow(r_pos, ge.x) : 0.0);
             uint32_t c[4] = {static_cast<uint32_t>(path), static_cast<uint32_t>(path >> 32),
                              static_cast<uint32_t>(s), 0x48534d43u};
             philox10(c, k0, k1);
@@ -64,8 +68,8 @@ __global__ void __launch_bounds__(256) k_mc(McParams mp, const double* __restric
             const double dz = mp.rho * dw + mp.sq1mr2 * (rad * sn);  // correlated_normals
             x += (-mp.kappa * x + y) * mp.dt + eta * mp.sqrt_dt * dw;
             y = y * mp.decay_y + eta * eta * mp.dt * mp.decay_h;
-            v += mp.theta * (1.0 - v_pos) * mp.dt + mp.eps * sqrt(v_pos) * mp.sqrt_dt * dz;
-            const double r_next = x + __ldg(f_next + s);
+            v += mp.theta * (1.0 - v_pos) * mp.dt + ge.y * sqrt(v_pos) * mp.sqrt_dt * dz;
+            const double r_next = x + fl.x;
             integral_r += 0.5 * (r + r_next) * mp.dt;
             r = r_next;
         }
@@ -97,9 +101,9 @@ __global__ void __launch_bounds__(256) k_mc(McParams mp, const double* __restric
 
 }  // namespace
 
-void mc_simulate(const McParams& mp, const double* f_next, double* partial, int blocks,
+void mc_simulate(const McParams& mp, const double* steps, double* partial, int blocks,
                  cudaStream_t stream) {
-    k_mc<<<blocks, 256, 0, stream>>>(mp, f_next, partial);
+    k_mc<<<blocks, 256, 0, stream>>>(mp, steps, partial);
 }
 
 }  // namespace hjmsv_b200

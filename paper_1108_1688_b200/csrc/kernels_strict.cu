@@ -32,7 +32,7 @@ __device__ __forceinline__ G coeff(const ProblemConst& pc, const Tab& T, double 
     const double v = T.vz[j];
     const double yt = T.yz[k];
     const double h1 = T.a[i] * v;
-    const double h2 = pc.half_eps2 * v;
+    const double h2 = T.heps2 * v;
     const double jr = T.rj1[i], jv = T.vj1[j];
     G g;
     g.g1 = h1 / (jr * jr);
@@ -58,7 +58,7 @@ __global__ void k_explicit(BatchView v, int s) {
     const int j = static_cast<int>((q / ny) % nv);
     const int i = static_cast<int>(q / (static_cast<long long>(ny) * nv));
     const ProblemConst& pc = v.pc[p];
-    const Tab T = tables(v, p);
+    const Tab T = tables(v, p, s);
     const double* step = step_row(v, p, s);
     const double* U = v.U + static_cast<size_t>(p) * v.N;
     double* D = v.D + static_cast<size_t>(p) * v.N;
@@ -182,7 +182,7 @@ __global__ void k_sweep(BatchView v, int s) {
     if (AX == AX_V && is_dirichlet(v, pc, i, 1, k)) return;
     if (AX == AX_Y && ny > 1 && is_dirichlet(v, pc, i, j, 1)) return;
 
-    const Tab T = tables(v, p);
+    const Tab T = tables(v, p, s);
     const double c4 = step_row(v, p, s)[ST_C4];
     const double th = pc.theta_dt;
     const long long base = static_cast<long long>(i) * nv * ny + static_cast<long long>(j) * ny + k;
@@ -305,7 +305,7 @@ __global__ void k_update(BatchView v, int s) {
         const double ad = fabs(dq);
         if (ad > 0.0) md = static_cast<unsigned long long>(__double_as_longlong(ad));
         const int face = dirichlet_face(v, pc, i, j, k);
-        if (face >= 0) un = face_value(pc, step_row(v, p, s), tables(v, p), face, i, k);
+        if (face >= 0) un = face_value(pc, step_row(v, p, s), tables(v, p, s), face, i, k);
         U[q] = un;
         // guard_finite (solver.cpp:69-77)
         if (!isfinite(un)) {

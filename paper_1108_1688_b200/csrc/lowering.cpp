@@ -35,11 +35,13 @@ void validate_config(const hjmsv_solver_config& c) {  // solver.cpp:10-20
         throw std::invalid_argument("divergence_bound must be positive");
 }
 
-void validate_model(const hjmsv_model& m) {  // model.cpp:25-33
+void validate_model(const hjmsv_model& m) {  // model.cpp:25-37
     if (m.kappa < 0.0) throw std::invalid_argument("kappa must be nonnegative");
     if (m.theta < 0.0) throw std::invalid_argument("theta must be nonnegative");
     if (m.rho < -1.0 || m.rho > 1.0) throw std::invalid_argument("rho must lie in [-1,1]");
-    if (m.gamma <= 0.0 || m.gamma > 1.0) throw std::invalid_argument("gamma must lie in (0,1]");
+    // a model function is checked at t = 0 only, as ModelParams::validate does
+    const double g = m.gamma_fn ? m.gamma_fn(0.0, m.fn_user) : m.gamma;
+    if (g <= 0.0 || g > 1.0) throw std::invalid_argument("gamma must lie in (0,1]");
 }
 
 Axis import_axis(const hjmsv_axis& a) {
@@ -153,6 +155,46 @@ void caplet_terminal(Lowered& L, const hjmsv_problem& p, const hjmsv_solver_conf
 }
 
 }  // namespace
+
+bool time_dependent(const hjmsv_model& m) { return m.lambda_fn || m.gamma_fn || m.eps_fn; }
+
+ModelAt model_at(const hjmsv_model& m, double t) {
+    // HjmCoefficientField::prepare's calls, in its order (discretization.cpp:41-43)
+    ModelAt x;
+    x.lambda = m.lambda_fn ? m.lambda_fn(t, m.fn_user) : m.lambda;
+    x.gamma = m.gamma_fn ? m.gamma_fn(t, m.fn_user) : m.gamma;
+    x.eps = m.eps_fn ? m.eps_fn(t, m.fn_user) : m.eps;
+    return x;
+}
+
+void prepare_ab(const Lowered& L, const ModelAt& x, double* a, double* b) {
+    // discretization.cpp:48-53, same operations
+    const double r0_pow = std::pow(L.r0, x.gamma - 1.0);
+    for (int i = 0; i < L.nr; ++i) {
+        const double rp = L.r.z[i] > 0.0 ? std::pow(L.r.z[i], x.gamma) * r0_pow : 0.0;
+        a[i] = 0.5 * x.lambda * x.lambda * rp * rp;
+        b[i] = x.lambda * x.eps * L.model.rho * rp;
+    }
+}
+
+void build_model_steps(Lowered& L) {
+    const int S = static_cast<int>(L.steps.size() / kStepStride);
+    if (!L.timedep) {
+        for (int s = 0; s < S; ++s) L.steps[static_cast<size_t>(s) * kStepStride + ST_HEPS2] = L.pc.half_eps2;
+        L.ab_steps.clear();
+        return;
+    }
+    const int nr = L.nr;
+    L.ab_steps.assign(static_cast<size_t>(S) * 2 * nr, 0.0);
+    for (int s = 0; s < S; ++s) {
+        double* e = &L.steps[static_cast<size_t>(s) * kStepStride];
+        // prepare(t_mid) (solver.cpp:96): the model functions at the half level
+        const ModelAt x = model_at(L.model, e[ST_TMID]);
+        e[ST_HEPS2] = 0.5 * x.eps * x.eps;
+        double* ab = &L.ab_steps[static_cast<size_t>(s) * 2 * nr];
+        prepare_ab(L, x, ab, ab + nr);
+    }
+}
 
 std::vector<double> march_levels(double maturity, int n_steps, int time_levels) {
     const double dt = maturity / n_steps;
@@ -322,14 +364,13 @@ Lowered lower_problem(const hjmsv_problem& p, const hjmsv_solver_config& cfg, in
     put(L.r.z); put(L.r.j1); put(L.r.j2);
     put(L.v.z); put(L.v.j1); put(L.v.j2);
     put(L.y.z); put(L.y.j1); put(L.y.j2);
-    const double r0_pow = std::pow(p.r0, m.gamma - 1.0);
-    for (int i = 0; i < nr; ++i) {
-        const double rp = L.r.z[i] > 0.0 ? std::pow(L.r.z[i], m.gamma) * r0_pow : 0.0;
-        t[i] = 0.5 * m.lambda * m.lambda * rp * rp;   // a_i
-        t[nr + i] = m.lambda * m.eps * m.rho * rp;     // b_i
-    }
+    L.model = m;
+    L.timedep = time_dependent(m);
+    // constant model: prepare's a_i, b_i once (a time-dependent one gets them per step)
+    if (!L.timedep) prepare_ab(L, model_at(m, 0.0), t, t + nr);
 
     build_step_table(L, march_levels(p.maturity, L.n_steps, p.time_levels), L.dt, true);
+    build_model_steps(L);
 
     // price readout at natural_spot (instruments.cpp:50-52, 145-149)
     const double f0 = L.curve.forward(0.0);
@@ -365,7 +406,7 @@ Lowered lower_problem(const hjmsv_problem& p, const hjmsv_solver_config& cfg, in
 }
 
 std::vector<double> build_fast_tables(const Lowered& L, const hjmsv_solver_config& cfg,
-                                      double th) {
+                                      double th, int step) {
     const int nr = L.nr, nv = L.nv, ny = L.ny;
     std::vector<double> t(fast_table_stride(nr, nv, ny), 0.0);
     double* R = t.data();
@@ -381,8 +422,13 @@ std::vector<double> build_fast_tables(const Lowered& L, const hjmsv_solver_confi
     // 0 < i < nr-1, 0 < j < nv-1, discretization.cpp:357-361); a singleton v axis has none
     const double inv_cross = (nr > 1 && nv > 1) ? 0.25 / (dxr * dxv) : 0.0;
     const ProblemConst& pc = L.pc;
-    const double* a = L.axes.data() + 3 * nr + 3 * nv + 3 * ny;
+    // prepare(t_mid)'s a_i, b_i and eps^2/2: the constants, or step `step`'s values
+    const bool per_step = L.timedep && step >= 0;
+    const double* a = per_step ? &L.ab_steps[static_cast<size_t>(step) * 2 * nr]
+                               : L.axes.data() + 3 * nr + 3 * nv + 3 * ny;
     const double* b = a + nr;
+    const double half_eps2 = per_step ? L.steps[static_cast<size_t>(step) * kStepStride + ST_HEPS2]
+                                      : pc.half_eps2;
     for (int i = 0; i < nr; ++i) {
         const double jr = L.r.j1[i];
         double* e = R + kFR * i;
@@ -399,8 +445,8 @@ std::vector<double> build_fast_tables(const Lowered& L, const hjmsv_solver_confi
         const double v = L.v.z[j], jv = L.v.j1[j];
         double* e = V + kFV * j;
         e[FV_V] = v;
-        e[FV_G2] = pc.half_eps2 * v / (jv * jv) * inv_dxv2;
-        e[FV_G5] = (pc.theta * (1.0 - v) / jv - pc.half_eps2 * v * L.v.j2[j] / (jv * jv * jv)) *
+        e[FV_G2] = half_eps2 * v / (jv * jv) * inv_dxv2;
+        e[FV_G5] = (pc.theta * (1.0 - v) / jv - half_eps2 * v * L.v.j2[j] / (jv * jv * jv)) *
                    inv_2dxv;
         e[FV_G3] = v / jv;
     }
@@ -484,8 +530,15 @@ McSetup lower_mc(const hjmsv_problem& p, const hjmsv_mc_config& c) {
     m.sqrt_dt = std::sqrt(m.dt);
     m.decay_y = std::exp(-2.0 * p.model.kappa * m.dt);
     m.decay_h = std::exp(-p.model.kappa * m.dt);
-    m.f_next.resize(m.n_steps);
-    for (int s = 0; s < m.n_steps; ++s) m.f_next[s] = curve.forward(s * m.dt + m.dt);
+    m.steps.resize(4 * static_cast<size_t>(m.n_steps));
+    for (int s = 0; s < m.n_steps; ++s) {
+        // run_path's per-step model functions at t = s dt (montecarlo.cpp:54-58)
+        const ModelAt x = model_at(p.model, s * m.dt);
+        m.steps[4 * s] = curve.forward(s * m.dt + m.dt);
+        m.steps[4 * s + 1] = x.lambda;
+        m.steps[4 * s + 2] = x.gamma;
+        m.steps[4 * s + 3] = x.eps;
+    }
     return m;
 }
 

@@ -24,7 +24,22 @@ struct Lowered {
     long long spot_idx[8] = {};  // interpolate_at corners at natural_spot
     double spot_w[8] = {};
     TermParam term{};            // terminal built on the device (kind != TERM_HOST)
+    hjmsv_model model{};         // ModelParams (with the model functions, if any)
+    bool timedep = false;        // lambda/gamma/eps given as functions of t
+    std::vector<double> ab_steps;  // timedep: n_steps * [a_i (nr), b_i (nr)] of prepare(t_mid)
 };
+
+/// lambda(t), gamma(t), eps(t) of a model (constants unless *_fn is set).
+struct ModelAt {
+    double lambda, gamma, eps;
+};
+bool time_dependent(const hjmsv_model& m);
+ModelAt model_at(const hjmsv_model& m, double t);
+/// prepare's a_i = lambda^2 rp^2 / 2, b_i = lambda eps rho rp (discretization.cpp:48-53).
+void prepare_ab(const Lowered& L, const ModelAt& x, double* a, double* b);
+/// Per-step model data from the step table's half levels: eps^2/2 into ST_HEPS2
+/// and, for model functions, the a_i / b_i of every step (L.ab_steps).
+void build_model_steps(Lowered& L);
 
 /// How lower_problem provides the terminal level: on the host (L.init) or as
 /// device terminal parameters (L.term) for ZCB / caplet problems without an
@@ -56,14 +71,15 @@ hjmsv_solver_config default_config();
 struct McSetup {
     int n_steps = 0;
     double dt = 0.0, sqrt_dt = 0.0, decay_y = 0.0, decay_h = 0.0, f0 = 0.0;
-    std::vector<double> f_next;   // f(0, (s+1) dt), s = 0..n_steps-1
+    std::vector<double> steps;    // per step s: f(0, (s+1) dt), lambda(s dt), gamma(s dt), eps(s dt)
     int caplet = 0;
     double accrual = 0.0, ratio = 0.0, g = 0.0, horizon = 0.0;
 };
 McSetup lower_mc(const hjmsv_problem& p, const hjmsv_mc_config& c);
 
 /// FAST-mode factor tables (layout: FastR/FastV/FastY in device_types.hpp).
+/// step >= 0 with model functions: the tables of that step's prepare(t_mid).
 std::vector<double> build_fast_tables(const Lowered& L, const hjmsv_solver_config& cfg,
-                                      double theta_dt);
+                                      double theta_dt, int step = -1);
 
 }  // namespace hjmsv_b200

@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes
 import math
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import Callable, Optional, Sequence
 
 import numpy as np
 
@@ -101,6 +101,11 @@ class ProblemSpec:
     face_rule: Sequence[int] = (1, 0, 1, 0, 2, 0)
     face_value: Sequence[tuple] = ((0, 0, 0, 0, 0),) * 6   # (kind, a, t1, b, t2)
     initial_grid: Optional[np.ndarray] = None
+    # time-dependent model functions lambda(t), gamma(t), eps(t) (ModelParams::
+    # lambda_fn / gamma_fn / eps_fn, model.hpp:22-24); None -> the constant above
+    lambda_fn: Optional[Callable[[float], float]] = None
+    gamma_fn: Optional[Callable[[float], float]] = None
+    eps_fn: Optional[Callable[[float], float]] = None
     _keep: list = field(default_factory=list, repr=False)
 
     @property
@@ -115,6 +120,15 @@ class ProblemSpec:
         p = A.CProblem()
         p.r, p.v, p.y = self.r.to_c(), self.v.to_c(), self.y.to_c()
         p.model = A.CModel(self.kappa, self.lam, self.gamma, self.eps, self.theta, self.rho)
+        fns = []
+        for name in ("lambda_fn", "gamma_fn", "eps_fn"):
+            f = getattr(self, name)
+            if f is not None:
+                # the C callback must outlive the C struct: kept with the spec
+                cb = A.TIME_FN(lambda t, _u, f=f: float(f(t)))
+                fns.append(cb)
+                setattr(p.model, name, cb)
+        self._fns = fns
         if self.curve_maturities is None:
             p.curve = A.CCurve(A.CURVE_FLAT, self.flat_base, 0, _ptr(None), _ptr(None))
         else:

@@ -91,3 +91,16 @@ def make_config(config_id: int, count: int | None = None, **overrides) -> List[P
 def solver_config() -> SolverConfig:
     """SolverConfig defaults (solver.hpp:10-20): theta 0.5, orders 2, smoothing m=3, bound 1e6."""
     return SolverConfig()
+
+
+def with_model_functions(p: ProblemSpec, amp: float = 0.3) -> ProblemSpec:
+    """The same problem with deterministic time-dependent model functions in
+    place of the constants (ModelParams::lambda_fn / gamma_fn / eps_fn,
+    model.hpp:22-24): a periodic volatility level, a drifting elasticity and a
+    decaying vol-of-variance around the drawn values. Not a BASELINE config —
+    the parity case for prepare(t)'s per-step evaluation (discretization.cpp:40-54)."""
+    lam0, gam0, eps0 = p.lam, p.gamma, p.eps
+    p.lambda_fn = lambda t: lam0 * (1.0 + amp * math.sin(2.0 * t))
+    p.gamma_fn = lambda t: gam0 - 0.05 * (1.0 - math.cos(t))
+    p.eps_fn = lambda t: eps0 * math.exp(-0.1 * t)
+    return p

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in declared_functions() if not hasattr(lib, n)]
     assert not missing, missing
     assert set(declared_functions()) == set(A.SIGNATURES), "ctypes table out of sync with header"
-    assert lib.hjmsv_abi_version() == 1
+    assert lib.hjmsv_abi_version() == 2  # hjmsv_model gained the model functions of t
 
 
 def test_library_is_sm100a_native():

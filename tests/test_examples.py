@@ -25,8 +25,8 @@ def test_reference_shim_matches_reference_run(gpu):
     out = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
-    assert {(r["case"], r["mode"]) for r in rows} == {("zcb", "strict"), ("zcb", "fast"),
-                                                      ("caplet", "strict"), ("caplet", "fast")}
+    assert {(r["case"], r["mode"]) for r in rows} == {
+        (c, m) for c in ("zcb", "caplet", "caplet_timefn") for m in ("strict", "fast")}
     for r in rows:
         assert r["grid_rel"] <= 1e-10 and r["price_rel"] <= 1e-10, r
 

@@ -426,3 +426,57 @@ def test_diagnostic_schedules(gpu, env):
     assert out.returncode == 0, out.stderr[-2000:]
     worst = float(out.stdout.split("WORST")[-1])
     assert worst <= TOL, (env, worst)
+
+
+# ---- time-dependent model functions lambda(t), gamma(t), eps(t) (model.hpp:22-24):
+# per-step coefficient tables from prepare(t_mid) (discretization.cpp:40-54)
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("shape", [(32, 32, 32), (24, 12, 16), (64, 32, 32)])
+def test_model_functions_march(gpu, oracle, mode, shape):
+    nr, nv, ny = shape
+    for cfg, idx in ((0, 4), (2, 6)):
+        p = W.with_model_functions(W.make_problem(cfg, idx, nr=nr, nv=nv, ny=ny, steps=40))
+        grids, prices, reps, _ = solve([p], mode)
+        g_ref, rep_ref = assert_parity(p, grids[0], prices[0], oracle, mode)
+        assert abs(reps[0]["last_max_delta"] - rep_ref["last_max_delta"]) <= 1e-10 * rep_ref["last_max_delta"]
+        # the functions matter: the constant model is measurably different
+        q = W.make_problem(cfg, idx, nr=nr, nv=nv, ny=ny, steps=40)
+        assert B.normwise_rel(oracle.run(q)[0], g_ref) > 1e-6
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_model_functions_mixed_batch(gpu, oracle, mode):
+    """A batch mixing constant and time-dependent models (every problem then
+    carries per-step tables)."""
+    probs = [W.make_problem(4, q, steps=50) for q in range(4)]
+    probs[1] = W.with_model_functions(probs[1])
+    probs[3] = W.with_model_functions(probs[3], amp=-0.2)
+    grids, prices, reps, _ = solve(probs, mode)
+    for q, p in enumerate(probs):
+        assert_parity(p, grids[q], prices[q], oracle, mode)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_model_functions_stages(gpu, oracle, mode):
+    p = W.with_model_functions(W.make_problem(2, 2, nr=24, nv=12, ny=16, steps=10))
+    rng = np.random.default_rng(5)
+    u = oracle.initial_level(p) * (1 + 1e-4 * rng.standard_normal(p.shape))
+    for t in (p.maturity, 0.37 * p.maturity):
+        f_ref = oracle.apply_operator(p, t, u)
+        assert B.normwise_rel(hj.apply_operator(p, t, u, mode=mode), f_ref) <= tol_for(mode) * 10
+    dt = p.maturity / 10
+    ref, md_ref, code, _ = oracle.douglas_step(p, u, 0.6 * p.maturity, dt)
+    out, md = hj.douglas_step(p, u, 0.6 * p.maturity, dt, mode=mode)
+    assert code == 0 and B.normwise_rel(out, ref) <= tol_for(mode)
+    assert abs(md - md_ref) <= 1e-10 * md_ref
+
+
+def test_model_functions_vs_compiled_reference(gpu, reference):
+    """FAST two-pass march with model functions against the compiled reference's run()."""
+    p = W.with_model_functions(W.make_problem(2, 9, nr=64, nv=32, ny=32, steps=60))
+    grids, prices, reps, _ = solve([p], "fast")
+    g_ref, rep_ref, code, _ = reference.run(p)
+    assert code == 0
+    assert B.normwise_rel(grids[0], g_ref) <= TOL
+    p_ref = reference.spot_price(p, g_ref)
+    assert abs(prices[0] - p_ref) <= TOL * abs(p_ref)

@@ -41,3 +41,14 @@ def test_device_mc_deterministic_and_zcb_discount(gpu, reference):
     assert a == b
     disc = reference.curve_eval(p, 0, np.array([p.maturity]))[0]
     assert abs(a[0] - disc) <= 4 * a[1] + 1e-4
+
+
+@pytest.mark.gpu
+def test_device_mc_model_functions(gpu, reference):
+    """run_path evaluates lambda(t), gamma(t), eps(t) at every step's start
+    (montecarlo.cpp:54-58); the device reads them from the per-step table."""
+    p = W.with_model_functions(W.make_problem(2, 3, nr=8, nv=4, ny=4, steps=4), amp=0.5)
+    m_d, se_d, _ = hj.mc_price(p, n_paths=100000, steps_per_year=48)
+    m_r, se_r, _ = reference.mc_price(p, n_paths=100000, steps_per_year=48)
+    tol = 4 * math.sqrt(se_d ** 2 + se_r ** 2)
+    assert abs(m_d - m_r) <= tol, f"{m_d} vs {m_r} (tol {tol:.2e})"

@@ -121,3 +121,38 @@ def test_greeks_restatement_bitexact_vs_reference(oracle, reference):
         r0_, v0_ = oracle.greeks(p, g, scale)
         r1_, v1_ = reference.greeks(p, g, scale)
         assert np.array_equal(r0_, r1_) and np.array_equal(v0_, v1_)
+
+
+@pytest.mark.parametrize("cfg,idx", [(0, 2), (2, 5), (4, 1)])
+def test_model_functions_bitexact_vs_reference(oracle, reference, cfg, idx):
+    """Time-dependent lambda(t), gamma(t), eps(t) (model.hpp:22-24): the
+    restatement evaluates them at every step's half level exactly as
+    HjmCoefficientField::prepare does (discretization.cpp:40-54)."""
+    p = W.with_model_functions(W.make_problem(cfg, idx, nr=20, nv=10, ny=12, steps=25))
+    g0, r0, c0, _ = oracle.run(p)
+    g1, r1, c1, _ = reference.run(p)
+    assert c0 == c1 == 0
+    assert np.array_equal(g0, g1)
+    assert r0["last_max_delta"] == r1["last_max_delta"]
+    # and the model functions matter
+    q = W.make_problem(cfg, idx, nr=20, nv=10, ny=12, steps=25)
+    assert not np.array_equal(g0, oracle.run(q)[0])
+
+
+def test_constant_model_functions_equal_constants(oracle, reference):
+    """Functions that return the constants give the constant model bit for bit."""
+    p = W.make_problem(2, 3, nr=16, nv=8, ny=10, steps=20)
+    g_const = oracle.run(p)[0]
+    lam, gam, eps = p.lam, p.gamma, p.eps
+    p.lambda_fn, p.gamma_fn, p.eps_fn = (lambda t: lam), (lambda t: gam), (lambda t: eps)
+    assert np.array_equal(oracle.run(p)[0], g_const)
+    assert np.array_equal(reference.run(p)[0], g_const)
+
+
+def test_model_function_validation(oracle, reference):
+    """ModelParams::validate checks gamma_fn(0) in (0,1] (model.cpp:36-37)."""
+    p = W.make_problem(0, 0, nr=12, nv=6, ny=6, steps=4)
+    p.gamma_fn = lambda t: 1.5 if t == 0.0 else 0.9
+    for lib in (oracle, reference):
+        g, rep, code, msg = lib.run(p, raise_on_error=False)
+        assert code == 1 and "gamma must lie in (0,1]" in msg
