@@ -1433,14 +1433,19 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int NV, int NY, bool SCAN, int KL = 16, int TPC = 1>
+template <int NV, int NY, bool SCAN, int KL = 16, int TPC = 1, bool PAD = false>
 __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     // launched as a programmatic dependent of the previous kernel: everything
     // below reads what it wrote (no-op without a programmatic dependency)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     tl_begin(v, s, 0);
     constexpr int M = 16;
-    constexpr int SR = NV * NY;
+    // PAD: any nv, any ny <= NY and any nr <= 512 (the reference's own meshes):
+    // the grid's real sizes are runtime values, k lanes past ny and rows past nr
+    // run inert (identity rows, no stores); otherwise NV x NY exactly
+    const int nyr = PAD ? v.ny : NY;
+    const int nvr = PAD ? v.nv : NV;
+    const int SR = PAD ? v.nv * v.ny : NV * NY;  // row stride (one r plane)
     extern __shared__ double sm[];
     const int S = blockDim.y;
     // KL consecutive k per segment group (16: one CTA of 16 S threads per SM on
@@ -1484,7 +1489,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         const unsigned rbytes = nr * kFR * sizeof(double), ybytes = 2 * nr * sizeof(double);
         bulk_init(tbar_s, rbytes + ybytes);
         bulk_copy(rt, F.R, rbytes, tbar_s);
-        bulk_copy(fy, v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY, ybytes, tbar_s);
+        bulk_copy(fy, v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * nyr, ybytes, tbar_s);
     }
     const double c4 = __ldg(step_row(v, p, s) + ST_C4);
     const double2* V2 = reinterpret_cast<const double2*>(F.V + kFV * j);
@@ -1497,7 +1502,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     // load-store-only path); j = 0 is Dirichlet (same path) or the degenerate
     // one-sided row (below)
     const bool vminD = dir(v, F_VMIN), vmaxD = dir(v, F_VMAX);
-    const bool jlo = j == 0, jhi = j == NV - 1;
+    const bool jlo = j == 0, jhi = j == nvr - 1;
     const bool jdir = (jhi && vmaxD) || (jlo && vminD);
     // the degenerate j = 0 row uses the interior stencil with its missing j-1
     // column replaced by j+1 and G2 replaced by G5: that is exactly the
@@ -1509,7 +1514,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
 
     // ---- per-tile (k-dependent) state, set by tile_setup(t)
     int k = 0;
-    bool k0 = false, kN = false, solve = false, kface = false, edge = false;
+    bool klive = true, k0 = false, kN = false, solve = false, kface = false, edge = false;
     int eoff = 0;
     double yk = 0.0, vs6 = 0.0, t6 = 0.0, ths = 0.0, rminv = 0.0, rmaxv = 0.0;
     const double* fyk = fy;
@@ -1517,10 +1522,13 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     auto tile_k = [&](int t) { return (kt0 + t) * KL + tx; };
     auto tile_setup = [&](int t) {
         k = tile_k(t);
+        klive = !PAD || k < nyr;
+        if (PAD && !klive) k = nyr - 1;  // inert lane: reads a real column, stores nothing
         k0 = k == 0;
-        kN = k == NY - 1;
+        kN = k == nyr - 1;
         // is_dirichlet(1,j,k) (solver.cpp:127): the column lies on a v or y Dirichlet face
-        solve = !(kN && ymaxD) && !(j == NV - 1 && dir(v, F_VMAX)) && !(k0 && yminD) && !(j == 0 && dir(v, F_VMIN));
+        solve = klive && !(kN && ymaxD) && !(j == nvr - 1 && dir(v, F_VMAX)) && !(k0 && yminD) &&
+                !(j == 0 && dir(v, F_VMIN));
         const double2* Y2 = reinterpret_cast<const double2*>(F.Y + kFY * k);
         const double2 y01 = __ldg(Y2), y23 = __ldg(Y2 + 1);  // (S6, T6), (Y, pad)
         yk = y23.x;
@@ -1529,12 +1537,12 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         fyk = fy + (kN ? 0 : nr);
         kface = (kN && ymaxD) || (k0 && yminD);
         // r-face values this thread needs (first / last segment)
-        rminv = (sg == 0 && rminD) ? __ldg(fbp + NY + k) : 0.0;
-        rmaxv = (a + M == nr && rmaxD) ? __ldg(fbp + k) : 0.0;
-        col = v.U + off + static_cast<size_t>(j) * NY + k;
+        rminv = (sg == 0 && rminD) ? __ldg(fbp + nyr + k) : 0.0;
+        rmaxv = ((PAD ? (a <= nr - 1 && nr - 1 < a + M) : a + M == nr) && rmaxD) ? __ldg(fbp + k) : 0.0;
+        col = v.U + off + static_cast<size_t>(j) * nyr + k;
         // the KL-lane group's edge lanes also carry their outside neighbour in k
         // (k-1 at tx 0, k+1 at tx KL-1; k+2 at k = 0 for the one-sided row)
-        edge = tx == 0 || (tx == KL - 1 && !kN);
+        edge = klive && (tx == 0 || (tx == KL - 1 && !kN));
         eoff = tx == 0 ? (k0 ? 2 : -1) : 1;
         // interior rows (0 < i < nr-1); a column that is not solved runs identity rows
         ths = solve ? th : 0.0;
@@ -1557,41 +1565,41 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     auto wslot = [&](int q, int c) { return myring + kRing * 4 + q * 4 + c; };
     // the j-1 column offset is a compile-time constant in each instantiation
     auto ring_rows = [&](auto jd, const double* cb, bool ed, int eo) {
-        constexpr int OFFM = decltype(jd)::value ? NY : -NY;
+        const int OFFM = decltype(jd)::value ? nyr : -nyr;
 #pragma unroll
         for (int r = 0; r < kRing; ++r) {
             const double* g = gptr_c(cb, a + 2 + r);
             cp_async8s(myring_s + 8 * (r * 4 + 0), g + OFFM);
             cp_async8s(myring_s + 8 * (r * 4 + 1), g);
-            cp_async8s(myring_s + 8 * (r * 4 + 2), g + NY);
+            cp_async8s(myring_s + 8 * (r * 4 + 2), g + nyr);
             if (ed) cp_async8s(myring_s + 8 * (r * 4 + 3), g + eo);
             cp_async_commit();
         }
     };
     auto prologue = [&](auto jd) {
-        constexpr int OFFM = decltype(jd)::value ? NY : -NY;
+        const int OFFM = decltype(jd)::value ? nyr : -nyr;
         const double* q = gptr(a - 1);
         m1 = __ldg(q);
-        mx = __ldg(q + NY) - __ldg(q + OFFM);
+        mx = __ldg(q + nyr) - __ldg(q + OFFM);
         q = gptr(a);
-        c0 = __ldg(q + OFFM); c1 = __ldg(q); c2 = __ldg(q + NY);
+        c0 = __ldg(q + OFFM); c1 = __ldg(q); c2 = __ldg(q + nyr);
         if (edge) ce = __ldg(q + eoff);
         q = gptr(a + 1);
-        p0 = __ldg(q + OFFM); p1 = __ldg(q); p2 = __ldg(q + NY);
+        p0 = __ldg(q + OFFM); p1 = __ldg(q); p2 = __ldg(q + nyr);
         if (edge) pe = __ldg(q + eoff);
         ring_rows(jd, col, edge, eoff);
     };
     // STAGE: the window rows a-1, a, a+1 of the tile at cb as one cp.async group
     // into the staging slots, then its ring rows (kRing groups)
     auto prologue_staged = [&](auto jd, const double* cb, bool ed, int eo) {
-        constexpr int OFFM = decltype(jd)::value ? NY : -NY;
+        const int OFFM = decltype(jd)::value ? nyr : -nyr;
         const unsigned ws = myring_s + 8 * (kRing * 4);
 #pragma unroll
         for (int w = 0; w < 3; ++w) {
             const double* g = gptr_c(cb, a - 1 + w);
             cp_async8s(ws + 8 * (w * 4 + 0), g + OFFM);
             cp_async8s(ws + 8 * (w * 4 + 1), g);
-            cp_async8s(ws + 8 * (w * 4 + 2), g + NY);
+            cp_async8s(ws + 8 * (w * 4 + 2), g + nyr);
             if (w > 0 && ed) cp_async8s(ws + 8 * (w * 4 + 3), g + eo);
         }
         cp_async_commit();
@@ -1629,13 +1637,14 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
 #pragma unroll 1
         for (int t = 0; t < TPC; ++t) {
             if (t > 0) tile_setup(t);
-            const double* fv = fbp + 2 * NY + 2 * nr + (jhi ? 0 : nr * NY) + k;
-            double* dcol = v.D + off + static_cast<size_t>(j) * NY + k;
+            const double* fv = fbp + 2 * nyr + 2 * nr + (jhi ? 0 : nr * nyr) + k;
+            double* dcol = v.D + off + static_cast<size_t>(j) * nyr + k;
 #pragma unroll 4
             for (int r = 0; r < M; ++r) {
                 const int i = a + r;
+                if (PAD && (i >= nr || !klive)) break;
                 const double u0 = __ldg(col + static_cast<size_t>(i) * SR);
-                double f = __ldg(fv + static_cast<size_t>(i) * NY);
+                double f = __ldg(fv + static_cast<size_t>(i) * nyr);
                 if (!jhi) {  // v_min ranks last
                     if (i == 0 && rminD) f = rminv;
                     if (k0 && yminD) f = fyk[i];
@@ -1693,7 +1702,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         int bad_r = 0;
         bool ok = true;
         auto march = [&](auto jd) {
-            constexpr int OFFM = decltype(jd)::value ? NY : -NY;
+            const int OFFM = decltype(jd)::value ? nyr : -nyr;
             // window for columns j-1 (0), j (1), j+1 (2): m = row ic-1, c = ic, p = ic+1;
             // rows ic+2 .. ic+1+kRing are in flight in this thread's ring slots
             // centre moves to row a+r: row a+r+1 comes out of ring slot (r-1) % kRing,
@@ -1714,7 +1723,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                     {
                     cp_async8s(myring_s + 8 * (q * 4 + 0), g + OFFM);
                     cp_async8s(myring_s + 8 * (q * 4 + 1), g);
-                    cp_async8s(myring_s + 8 * (q * 4 + 2), g + NY);
+                    cp_async8s(myring_s + 8 * (q * 4 + 2), g + nyr);
                     if (edge) cp_async8s(myring_s + 8 * (q * 4 + 3), g + eoff);
                     }
                     cp_async_commit();
@@ -1751,7 +1760,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             auto row = [&](int r, double& l, double& d, double& u) {
                 const int i = a + r;
                 double2 r01, r23, r45, r67;
-                rtab(i, r01, r23, r45, r67);
+                rtab(PAD ? min(i, nr - 1) : i, r01, r23, r45, r67);
                 const double g4h = g4(r01, r23, r45);
                 if (r == 0) {
                     if (a == 0) {
@@ -1800,10 +1809,16 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                     shift(r);
                     const double xv = stencil(true, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
                     // face plane i = nr-1: r_max is always Dirichlet and ranks first
-                    x[r] = (r == M - 1 && i == nr - 1 && rmaxD) ? rmaxv - c1 : xv;
+                    // (PAD: rows past nr-1 are inert identity rows)
+                    if constexpr (PAD) x[r] = xv;
+                    else x[r] = (r == M - 1 && i == nr - 1 && rmaxD) ? rmaxv - c1 : xv;
+                }
+                if constexpr (PAD) {  // the r_max face row anywhere in the segment; inert rows past it
+                    if (i == nr - 1 && rmaxD) x[r] = rmaxv - c1;
+                    else if (i >= nr) x[r] = 0.0;
                 }
                 // rows a+1 .. a+14 are always interior; a+15 may be the r_max face
-                if (r == M - 1 && i == nr - 1 && rmaxD) {
+                if (PAD ? (i >= nr - 1 && (i > nr - 1 || rmaxD)) : (r == M - 1 && i == nr - 1 && rmaxD)) {
                     l = 0.0; d = 1.0; u = 0.0;
                 } else {
                     interior(r01.x * vj, g4h, l, d, u);
@@ -1816,14 +1831,14 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             if constexpr (STAGE) {
                 if (t + 1 < TPC) {
                     const int kn = tile_k(t + 1);
-                    const bool ed = tx == 0 || (tx == KL - 1 && kn != NY - 1);
-                    prologue_staged(jd, v.U + off + static_cast<size_t>(j) * NY + kn, ed, tx == 0 ? -1 : 1);
+                    const bool ed = tx == 0 || (tx == KL - 1 && kn != nyr - 1);
+                    prologue_staged(jd, v.U + off + static_cast<size_t>(j) * nyr + kn, ed, tx == 0 ? -1 : 1);
                 }
             }
         };
         if (jdeg) march(std::true_type{});
         else march(std::false_type{});
-        if (!ok) record_pivot(st, s, 0, j * NY + k, a + bad_r);
+        if (!ok) record_pivot(st, s, 0, j * nyr + k, a + bad_r);
         // reduced-system rows as [column][field][segment] (field stride S+1, column
         // stride 8S+9: conflict-free for the writers, lanes = k, and for the
         // scans, lanes = segments)
@@ -1836,8 +1851,9 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                 const int cc = tid / S, ts = tid - cc * S;
                 double* Ec = red + cc * CST + ts;
                 const int kk = (kt0 + t) * KL + cc;
-                const bool csolve = !(kk == NY - 1 && ymaxD) && !(j == NV - 1 && dir(v, F_VMAX)) &&
-                                    !(kk == 0 && yminD) && !(j == 0 && dir(v, F_VMIN));
+                const bool csolve = (!PAD || kk < nyr) && !(kk == nyr - 1 && ymaxD) &&
+                                    !(j == nvr - 1 && dir(v, F_VMAX)) && !(kk == 0 && yminD) &&
+                                    !(j == 0 && dir(v, F_VMIN));
                 const double eyF = Ec[0], eaF = Ec[FS], ebF = Ec[2 * FS], eyL = Ec[3 * FS], eaL = Ec[4 * FS],
                              ebL = Ec[5 * FS];
                 double lf = 0.0, rg = 0.0;
@@ -1845,7 +1861,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                 if (S == 16) bad = reduced_scan<16>(eyF, eaF, ebF, eyL, eaL, ebL, ts, S, lf, rg);
                 else bad = reduced_scan<32>(eyF, eaF, ebF, eyL, eaL, ebL, ts, S, lf, rg);
                 if (v.dbg & 1) lf = rg = 0.0;  // diagnostic: uncoupled segments (wrong results, finite)
-                if (csolve && bad) record_pivot(st, s, 0, j * NY + kk, bad * M);
+                if (csolve && bad) record_pivot(st, s, 0, j * nyr + kk, bad * M);
                 Ec[6 * FS] = lf;  // x_{a-1} of segment ts
                 Ec[7 * FS] = rg;  // x_{a+m} of segment ts
             } else if (KL == 16 && sg < 2) {  // warp 0: segment rows 0 (forward) and 1 (backward) of every column
@@ -1853,7 +1869,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                 if (solve) {
                     int bt = 0;
                     if (!reduced_solve_2way(red + tx * CST, S, 1, FS, sg == 1, mask, 16, bt))
-                        record_pivot(st, s, 0, j * NY + k, bt * M);
+                        record_pivot(st, s, 0, j * nyr + k, bt * M);
                     __syncwarp(mask);
                     // p_t, q_t -> each segment's left (p_{t-1}) / right (q_t), as the scan leaves them
                     if (sg == 0) {
@@ -1875,16 +1891,18 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
 #pragma unroll
             for (int r = 0; r < M; ++r) {
                 const int i = a + r;
+                if (PAD && i >= nr) break;
                 if (!((i == nr - 1 && rmaxD) || (i == 0 && rminD && !(kN && ymaxD))))
                     x[r] = fyk[i] - __ldg(col + static_cast<size_t>(i) * SR);
             }
         }
         double b = bL;
-        double* __restrict__ dcol = v.D + off + static_cast<size_t>(j) * NY + k + static_cast<size_t>(a) * SR;
+        double* __restrict__ dcol = v.D + off + static_cast<size_t>(j) * nyr + k + static_cast<size_t>(a) * SR;
 #pragma unroll
         for (int r = M - 1; r >= 0; --r) {
             if (r < M - 1) b = -cs[r] * b;
-            dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(al[r], left, x[r]));
+            if (!PAD || (klive && a + r < nr))
+                dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(al[r], left, x[r]));
         }
         if (TPC > 1 && t + 1 < TPC) __syncthreads();  // the reduced rows are reused by the next tile
     }
@@ -1892,7 +1910,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
 }
 
 inline size_t pa_smem(int nr, int kl = 16, int tpc = 1) {
-    const int S = nr / 16, nt = kl * S;
+    const int S = (nr + 15) / 16, nt = kl * S;
     const int rst = kRing * 4 + (tpc > 1 ? 12 : 0) + 1;
     return sizeof(double) * (static_cast<size_t>(kl) * (8 * S + 9) + static_cast<size_t>(rst) * nt +
                              static_cast<size_t>(nr) * (kFR + 2));
@@ -2510,7 +2528,13 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         const char* e = std::getenv("HJMSV_PA");
         return e ? std::atoi(e) : 1;
     }();
-    const bool pa = pa_env && shape != 0 && v.nr % 16 == 0 && v.nr / 16 <= 32;
+    const bool pa_exact = pa_env && shape != 0 && v.nr % 16 == 0 && v.nr / 16 <= 32;
+    // any other shape with nv, ny >= 3, ny <= 256, nr <= 512 (e.g. the reference's own
+    // 100x50x50 caplet mesh) runs pass A padded: ny rounded up to 32/64/128/256,
+    // nr to a multiple of 16, the extra lanes and rows inert
+    const bool pa_pad = pa_env && !pa_exact && v.nv >= 3 && v.ny >= 3 && v.ny <= 256 && v.nr >= 3 &&
+                        v.nr <= 512;
+    const bool pa = pa_exact || pa_pad;
     // folding the face table into pass A pays off for single grids; a large
     // batch computes it faster as its own full-occupancy launch (measured)
     static const int fold_env = [] {
@@ -2523,7 +2547,31 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         k_faces<<<dim3((v.fb_stride + 255) / 256, v.P), 256, 0, stream>>>(v, s);
         mark(4, "fx_faces", 0.0);
     }
-    if (pa) {
+    if (pa_pad) {
+        // pass A fused (padded shapes): explicit stencil + r-lines
+        const int S = (v.nr + 15) / 16;
+        const int nyp = v.ny <= 32 ? 32 : v.ny <= 64 ? 64 : v.ny <= 128 ? 128 : 256;
+        const dim3 g(v.nv * (nyp / 16), v.P), b(16, S);
+        const size_t sm = pa_smem(v.nr);
+        const bool scan = (S == 16 || S == 32) && !(v.dbg & 2);
+        auto go = [&](auto kern) {
+            smem_attr(reinterpret_cast<const void*>(kern), sm);
+            launch_pdl(kern, g, b, sm, stream, v, s);
+        };
+        switch (nyp) {
+            case 32: go(k_pa<0, 32, false, 16, 1, true>); break;
+            case 64: go(k_pa<0, 64, false, 16, 1, true>); break;
+            case 128:
+                if (scan) go(k_pa<0, 128, true, 16, 1, true>);
+                else go(k_pa<0, 128, false, 16, 1, true>);
+                break;
+            default:
+                if (scan) go(k_pa<0, 256, true, 16, 1, true>);
+                else go(k_pa<0, 256, false, 16, 1, true>);
+                break;
+        }
+        mark(0, "fx_explicit_sweep_r", 16.0);
+    } else if (pa) {
         // pass A fused: explicit stencil + r-lines
         const int S = v.nr / 16;
         // k-lane group width: 8 for 512-row lines (two 256-thread CTAs per SM

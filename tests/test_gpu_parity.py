@@ -480,3 +480,19 @@ def test_model_functions_vs_compiled_reference(gpu, reference):
     assert B.normwise_rel(grids[0], g_ref) <= TOL
     p_ref = reference.spot_price(p, g_ref)
     assert abs(prices[0] - p_ref) <= TOL * abs(p_ref)
+
+
+@pytest.mark.parametrize("shape", [(100, 50, 50), (72, 40, 90), (130, 33, 64), (40, 24, 200), (20, 130, 17)])
+def test_padded_pass_a_shapes(gpu, oracle, shape):
+    """Shapes outside the exact instantiations run the fused pass A padded (ny up
+    to 32/64/128/256 and nr up to a multiple of 16 with inert lanes and rows),
+    e.g. the reference's own 100x50x50 caplet mesh (instruments.cpp:11-22)."""
+    nr, nv, ny = shape
+    p = W.make_problem(2, 11, nr=nr, nv=nv, ny=ny, steps=40)
+    with hj.Solver([p], mode="fast") as s:
+        prof, _ = s.kernel_profile(2)
+        assert "fx_explicit_sweep_r" in [k["name"] for k in prof]
+        s.reset()
+        s.run()
+        g, price = s.grid(0), float(s.spot_prices()[0])
+    assert_parity(p, g, price, oracle, "fast")
