@@ -1962,7 +1962,7 @@ struct PlaneGeom {
     __device__ static int ci(int t, int k) { return t * CP + k; }
 };
 
-template <int NV, int NY, int CS, int NTX, int MB>
+template <int NV, int NY, int CS, int NTX, int MB, bool PAD = false>
 __global__ void __launch_bounds__(NTX, (PlaneGeom<NV, NY, CS, NTX, MB>::MINB))
 k_plane(BatchView v, int s) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of pass A
@@ -1976,6 +1976,10 @@ k_plane(BatchView v, int s) {
     double* car = ytab + G::YT;      // [2][SV][NY]
     double* ey = car + G::CAR;       // [NT/LY lines][LY][8]
     const int nr = v.nr;
+    // PAD: an nv x ny plane (nv, ny <= NV = NY) in the padded tile; rows j >= nv and
+    // columns k >= ny are inert (identity lines, no loads or stores)
+    static_assert(!PAD || CS == 1, "padded planes fit one CTA");
+    const int nvr = PAD ? v.nv : NV, nyr = PAD ? v.ny : NY;
     const int tid = threadIdx.x;
     const int w = blockIdx.x / CS;
     const int c = CS > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
@@ -2001,7 +2005,7 @@ k_plane(BatchView v, int s) {
         }
     };
     const size_t off = static_cast<size_t>(p) * v.N;
-    const size_t pb = off + (static_cast<size_t>(i) * NV + j0) * NY;  // first row of this CTA
+    const size_t pb = off + (static_cast<size_t>(i) * nvr + j0) * nyr;  // first row of this CTA
     const FT F = ftab(v, p, s);
     // per-plane scalars, loaded while the plane is staged
     const ProblemConst& pc = v.pc[p];
@@ -2016,7 +2020,7 @@ k_plane(BatchView v, int s) {
     const int kc = tid % NY, sl0 = tid / NY;
     double xv[TPT][MS];
     {  // staged even for a failed problem: the loads need not wait for the status word
-        if (tid == 0) {  // U rows -> L2 early, so the update's loads hit L2
+        if (!PAD && tid == 0) {  // U rows -> L2 early, so the update's loads hit L2
             constexpr unsigned bytes = RV * NY * sizeof(double);
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.U + pb), "r"(bytes) : "memory");
         }
@@ -2025,8 +2029,18 @@ k_plane(BatchView v, int s) {
 #pragma unroll
             for (int q = 0; q < TPT; ++q)
 #pragma unroll
-                for (int r = 0; r < MS; ++r)
-                    xv[q][r] = __ldg(v.D + pb + static_cast<size_t>((sl0 + q * SSTEP) * MS + r) * NY + kc);
+                for (int r = 0; r < MS; ++r) {
+                    const int jr = (sl0 + q * SSTEP) * MS + r;
+                    if constexpr (PAD)
+                        xv[q][r] = (jr < nvr && kc < nyr) ? __ldg(v.D + pb + static_cast<size_t>(jr) * nyr + kc) : 0.0;
+                    else
+                        xv[q][r] = __ldg(v.D + pb + static_cast<size_t>(jr) * NY + kc);
+                }
+        } else if constexpr (PAD) {
+            for (int e = tid; e < RV * NY; e += NT) {
+                const int j = e / NY, k = e - (e / NY) * NY;
+                tile[G::at(j, k)] = (j < nvr && k < nyr) ? __ldg(v.D + pb + static_cast<size_t>(j) * nyr + k) : 0.0;
+            }
         } else {
             // stage the rows of dU1: all 128-bit loads in flight, then the smem stores
             constexpr int PER = RV * NY / 2 / NT;
@@ -2042,6 +2056,11 @@ k_plane(BatchView v, int s) {
             }
         }
         for (int e = tid; e < NV; e += NT) {
+            if (PAD && e >= nvr) {  // inert rows: identity v-line rows, decoupled
+                vtab[e] = 1.0;
+                vtab[NV + e] = vtab[2 * NV + e] = vtab[3 * NV + e] = vtab[4 * NV + e] = vtab[5 * NV + e] = 0.0;
+                continue;
+            }
             const double* Vr = F.V + kFV * e;
             vtab[e] = Vr[FV_RP];
             vtab[NV + e] = Vr[FV_B];
@@ -2051,13 +2070,13 @@ k_plane(BatchView v, int s) {
             vtab[5 * NV + e] = Vr[FV_V];
         }
         if (tid < 2)  // this plane's y-face values at t_next: YMAX, YMIN
-            vtab[6 * NV + tid] = __ldg(v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * NY + tid * nr + i);
+            vtab[6 * NV + tid] = __ldg(v.fb + static_cast<size_t>(p) * v.fb_stride + 2 * nyr + tid * nr + i);
         for (int e = tid; e < NY; e += NT) {  // padded so the segments hit distinct banks
             // scaled by theta dt: a y-row coefficient is one FMA, th g6 = h1 (th S6) + (th T6)
             const int cc = 2 * ((e >> 4) * 17 + (e & 15));
             const double thp = v.pc[p].theta_dt;
-            ytab[cc] = thp * F.Y[kFY * e + FY_S6];
-            ytab[cc + 1] = thp * F.Y[kFY * e + FY_T6];
+            ytab[cc] = (PAD && e >= nyr) ? 0.0 : thp * F.Y[kFY * e + FY_S6];
+            ytab[cc + 1] = (PAD && e >= nyr) ? 0.0 : thp * F.Y[kFY * e + FY_T6];
         }
     }
     __syncthreads();
@@ -2073,7 +2092,7 @@ k_plane(BatchView v, int s) {
         // registers (TPT independent chains per thread); segment end values go
         // to every CTA of the cluster, each CTA runs the (short) carry chains
         // itself; one store of dU2 into the tile
-        const bool colD = (kc == 0 && yminD) || (kc == NY - 1 && ymaxD);
+        const bool colD = (kc == 0 && yminD) || (kc == nyr - 1 && ymaxD) || (PAD && kc >= nyr);
         const bool vs = vwork && !colD && !(v.dbg & 16);  // cluster-uniform barriers below
         if (vwork) {
             int bad = -1;  // first singular v pivot (table NaN), warp-uniform
@@ -2082,7 +2101,7 @@ k_plane(BatchView v, int s) {
                 const unsigned m = __ballot_sync(0xffffffffu, isnan(vtab[jj + (tid & 31)]));
                 if (m && bad < 0) bad = jj + __ffs(m) - 1;
             }
-            if (bad >= 0 && vs && c == 0) record_pivot(st, s, 1, i * NY + kc, bad);
+            if (bad >= 0 && vs && c == 0) record_pivot(st, s, 1, i * nyr + kc, bad);
         }
         if (vs) {
 #pragma unroll
@@ -2157,7 +2176,7 @@ k_plane(BatchView v, int s) {
         // passes; measured faster for 32-row columns, slower for longer ones)
         if (vwork && tid < NY) {
             const int k = tid;
-            if (!((k == 0 && yminD) || (k == NY - 1 && ymaxD))) {
+            if (!((k == 0 && yminD) || (k == nyr - 1 && ymaxD) || (PAD && k >= nyr))) {
                 double loc = 0.0;
                 int bad = -1;
 #pragma unroll 8
@@ -2166,7 +2185,7 @@ k_plane(BatchView v, int s) {
                     loc = fma(vtab[NV + j], loc, vtab[j] * tile[G::at(j, k)]);
                     tile[G::at(j, k)] = loc;
                 }
-                if (bad >= 0) record_pivot(st, s, 1, i * NY + k, bad);
+                if (bad >= 0) record_pivot(st, s, 1, i * nyr + k, bad);
                 double xb = 0.0;
 #pragma unroll 8
                 for (int j = NV - 1; j >= 0; --j) {
@@ -2187,19 +2206,25 @@ k_plane(BatchView v, int s) {
     for (int h = 0; h < G::YROUNDS; ++h) {
         const int task = h * NT + tid;
         constexpr bool ALL_LIVE = (RV * LY) % NT == 0;  // every round full: no tail lanes
-        const bool live = ALL_LIVE || task < RV * LY;
-        const int jl = live ? task / LY : 0, sy = task % LY;
+        const int jl0 = (ALL_LIVE || task < RV * LY) ? task / LY : 0, sy = task % LY;
+        const bool live = (ALL_LIVE || task < RV * LY) && (!PAD || j0 + jl0 < nvr);
+        const int jl = live ? jl0 : 0;
         const int j = j0 + jl;
         const int a = sy * MS;
-        const bool solve = live && !planeD && !((j == 0 && vminD) || (j == NV - 1 && vmaxD));
-        double* up = v.U + pb + static_cast<size_t>(jl) * NY + a;
+        const bool solve = live && !planeD && !((j == 0 && vminD) || (j == nvr - 1 && vmaxD));
+        double* up = v.U + pb + static_cast<size_t>(jl) * nyr + a;
         double un[MS];
         auto load_u = [&] {
+            if constexpr (PAD) {  // rows of ny doubles: no 16-byte alignment, masked tail
 #pragma unroll
-            for (int q = 0; q < MS / 2; ++q) {
-                const double2 t = reinterpret_cast<const double2*>(up)[q];
-                un[2 * q] = t.x;
-                un[2 * q + 1] = t.y;
+                for (int r = 0; r < MS; ++r) un[r] = a + r < nyr ? up[r] : 0.0;
+            } else {
+#pragma unroll
+                for (int q = 0; q < MS / 2; ++q) {
+                    const double2 t = reinterpret_cast<const double2*>(up)[q];
+                    un[2 * q] = t.x;
+                    un[2 * q + 1] = t.y;
+                }
             }
         };
         // one CTA per SM (the 128- and 256-wide planes): the warp's rows of U
@@ -2209,7 +2234,7 @@ k_plane(BatchView v, int s) {
         // every lane has read its x; loads are in flight through the solve
         constexpr bool early_u = G::MINB == 1;       // registers for U in flight through the solve
         constexpr int WROWS = 32 / LY;
-        constexpr bool stage_u = WROWS * NY == 512 && ALL_LIVE;  // all benchmarked shapes
+        constexpr bool stage_u = WROWS * NY == 512 && ALL_LIVE && !PAD;  // all benchmarked shapes
         const int jw = jl & ~(WROWS - 1);  // the warp's first row
         const int ln = tid & 31;
         double2 us[stage_u ? 8 : 1];
@@ -2264,8 +2289,8 @@ k_plane(BatchView v, int s) {
             auto row = [&](int r, double& l, double& d, double& u) {
                 if (r == 0 && sy == 0) {
                     l = 0.0; d = f0d; u = f0u;
-                } else if (r == MS - 1 && lastI) {
-                    l = 0.0; d = 1.0; u = 0.0;
+                } else if (PAD ? (a + r >= nyr - 1 && (a + r > nyr - 1 || ymaxD)) : (r == MS - 1 && lastI)) {
+                    l = 0.0; d = 1.0; u = 0.0;  // the y_max face row (PAD: and the inert rows past it)
                 } else {
                     l = lr[r]; d = dint; u = -lr[r];
                 }
@@ -2275,7 +2300,7 @@ k_plane(BatchView v, int s) {
             bool sok;
             if constexpr (G::MINB == 1) sok = seg_solve_tw<MS>(x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
             else sok = seg_solve<MS>(MS, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
-            if (!sok) record_pivot(st, s, 2, i * NV + j, a + bad_r);
+            if (!sok) record_pivot(st, s, 2, i * nvr + j, a + bad_r);
         } else {  // a line that is not solved keeps dU: zero spikes and couplings
 #pragma unroll
             for (int r = 0; r < MS; ++r) cs[r] = al[r] = 0.0;
@@ -2296,7 +2321,7 @@ k_plane(BatchView v, int s) {
             __syncwarp();  // a line's LY segments lie in one warp
             if (solve && sy == 0) {
                 int bt = 0;
-                if (!reduced_solve(ew, LY, TS, bt, LPW)) record_pivot(st, s, 2, i * NV + j, bt * MS);
+                if (!reduced_solve(ew, LY, TS, bt, LPW)) record_pivot(st, s, 2, i * nvr + j, bt * MS);
             }
             __syncwarp();
             if (solve && sy > 0) left = e[-TS + 6 * LPW];
@@ -2310,7 +2335,7 @@ k_plane(BatchView v, int s) {
                 // the line's first vanishing reduced pivot (its lanes are g0 .. g0+LY-1)
                 const int g0 = (tid & 31) & ~(LY - 1);
                 const unsigned lm = (bm >> g0) & ((LY < 32) ? ((1u << LY) - 1u) : 0xffffffffu);
-                if (lm && sy == __ffs(lm) - 1) record_pivot(st, s, 2, i * NV + j, bt * MS);
+                if (lm && sy == __ffs(lm) - 1) record_pivot(st, s, 2, i * nvr + j, bt * MS);
                 if (sy > 0) left = lf;
                 if (sy < LY - 1) right = rg;
             }
@@ -2349,12 +2374,17 @@ k_plane(BatchView v, int s) {
             }
             if (!solve) {
 #pragma unroll
-                for (int r = 0; r < MS; ++r) un[r] = fval(v, p, dface(v, i, j, a + r), i, a + r);
+                for (int r = 0; r < MS; ++r)
+                    un[r] = (PAD && a + r >= nyr) ? 0.0 : fval(v, p, dface(v, i, j, a + r), i, a + r);
             } else {
                 if (sy == 0 && yminD) un[0] = vtab[6 * NV + 1];
-                if (sy == LY - 1 && ymaxD) un[MS - 1] = vtab[6 * NV];
+                if constexpr (PAD) {
+                    if (ymaxD && a <= nyr - 1 && nyr - 1 < a + MS) un[(nyr - 1) - a] = vtab[6 * NV];
+                } else {
+                    if (sy == LY - 1 && ymaxD) un[MS - 1] = vtab[6 * NV];
+                }
             }
-            if (!(v.dbg & 32)) guard_seg<MS>(v, p, s, (static_cast<size_t>(i) * NV + j) * NY + a, un, bound);
+            if (!(v.dbg & 32)) guard_seg<MS>(v, p, s, (static_cast<size_t>(i) * nvr + j) * nyr + a, un, bound);
             if constexpr (stage_u) {  // back through the tile rows, out as coalesced chunks
 #pragma unroll
                 for (int q = 0; q < MS / 2; ++q)
@@ -2366,6 +2396,10 @@ k_plane(BatchView v, int s) {
                     const int e = q * 64 + 2 * ln;
                     gw[q * 32 + ln] = *reinterpret_cast<const double2*>(tile + G::at(jw + e / NY, e % NY));
                 }
+            } else if constexpr (PAD) {
+#pragma unroll
+                for (int r = 0; r < MS; ++r)
+                    if (a + r < nyr) up[r] = un[r];
             } else {
 #pragma unroll
                 for (int q = 0; q < MS / 2; ++q)
@@ -2385,21 +2419,22 @@ k_plane(BatchView v, int s) {
         const double* stp = step_row(v, p, s + 1);
         const Tab T = tables(v, p, s);
         const bool rface = i == 0 || i == nr - 1;
-        const int n_ent = (c == 0 ? 2 : 0) + 2 * (NY / CS) + (rface && c == 0 ? NY : 0);
+        const int nyc = nyr / CS;  // this CTA's share of k
+        const int n_ent = (c == 0 ? 2 : 0) + 2 * nyc + (rface && c == 0 ? nyr : 0);
         for (int e = tid; e < n_ent; e += NT) {
             int face, k = 0, q;
-            if (e < 2 * (NY / CS)) {  // v faces: this CTA's share of k
-                face = e < NY / CS ? F_VMAX : F_VMIN;
-                k = c * (NY / CS) + (e < NY / CS ? e : e - NY / CS);
-                q = 2 * NY + 2 * nr + (face == F_VMAX ? 0 : nr * NY) + i * NY + k;
-            } else if (c == 0 && e < 2 * (NY / CS) + 2) {  // y faces
-                face = e == 2 * (NY / CS) ? F_YMAX : F_YMIN;
-                k = face == F_YMAX ? NY - 1 : 0;
-                q = 2 * NY + (face == F_YMAX ? 0 : nr) + i;
+            if (e < 2 * nyc) {  // v faces: this CTA's share of k
+                face = e < nyc ? F_VMAX : F_VMIN;
+                k = c * nyc + (e < nyc ? e : e - nyc);
+                q = 2 * nyr + 2 * nr + (face == F_VMAX ? 0 : nr * nyr) + i * nyr + k;
+            } else if (c == 0 && e < 2 * nyc + 2) {  // y faces
+                face = e == 2 * nyc ? F_YMAX : F_YMIN;
+                k = face == F_YMAX ? nyr - 1 : 0;
+                q = 2 * nyr + (face == F_YMAX ? 0 : nr) + i;
             } else {  // r faces of the boundary planes
                 face = i == nr - 1 ? F_RMAX : F_RMIN;
-                k = e - 2 * (NY / CS) - 2;
-                q = (face == F_RMAX ? 0 : NY) + k;
+                k = e - 2 * nyc - 2;
+                q = (face == F_RMAX ? 0 : nyr) + k;
             }
             fbn[q] = (v.dmask >> face & 1) ? face_value(v.pc[p], stp, T, face, i, k) : 0.0;
         }
@@ -2449,10 +2484,10 @@ void launch_pdl(K kernel, dim3 g, dim3 b, size_t sm, cudaStream_t stream, const 
     cudaLaunchKernelEx(&cfg, kernel, v, s);
 }
 
-template <int NV, int NY, int CS, int NT, int MB = 0>
+template <int NV, int NY, int CS, int NT, int MB = 0, bool PAD = false>
 void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
     using G = PlaneGeom<NV, NY, CS, NT, MB>;
-    smem_attr(reinterpret_cast<const void*>(k_plane<NV, NY, CS, NT, MB>), G::SMEM);
+    smem_attr(reinterpret_cast<const void*>(k_plane<NV, NY, CS, NT, MB, PAD>), G::SMEM);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(v.nr * v.P * CS);
     cfg.blockDim = dim3(NT);
@@ -2467,7 +2502,7 @@ void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
     at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    cudaLaunchKernelEx(&cfg, k_plane<NV, NY, CS, NT, MB>, v, s);
+    cudaLaunchKernelEx(&cfg, k_plane<NV, NY, CS, NT, MB, PAD>, v, s);
 }
 
 int plane_kernels() {
@@ -2523,7 +2558,14 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
     const int tk = (v.ny + 31) / 32, tj = (v.nv + 7) / 8;
     const int shape = specialised_shape(v);
     const int pl = plane_kernels();
-    const bool plane = pl && (shape == 32 || shape == 64 || shape == 128 || shape == 256);
+    const bool plane_exact = pl && (shape == 32 || shape == 64 || shape == 128 || shape == 256);
+    // any other plane up to 128 x 128 (nv, ny >= 3) runs pass B padded in a square
+    // 32 / 64 / 128 tile (inert rows and columns), after the padded pass A
+    const int pmax = std::max(v.nv, v.ny);
+    const int plane_pad = (pl && !plane_exact && v.nv >= 3 && v.ny >= 3 && pmax <= 128)
+                              ? (pmax <= 32 ? 32 : pmax <= 64 ? 64 : 128)
+                              : 0;
+    const bool plane = plane_exact || plane_pad;
     static const int pa_env = [] {
         const char* e = std::getenv("HJMSV_PA");
         return e ? std::atoi(e) : 1;
@@ -2652,7 +2694,10 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
     }
     if (plane) {
         // pass B fused: v-lines + y-lines + update on an SMEM-resident plane
-        if (shape == 32) launch_plane<32, 32, 1, 64>(v, s, stream);
+        if (plane_pad == 32) launch_plane<32, 32, 1, 64, 0, true>(v, s, stream);
+        else if (plane_pad == 64) launch_plane<64, 64, 1, 256, 0, true>(v, s, stream);
+        else if (plane_pad == 128) launch_plane<128, 128, 1, 256, 0, true>(v, s, stream);
+        else if (shape == 32) launch_plane<32, 32, 1, 64>(v, s, stream);
         else if (shape == 64) launch_plane<64, 64, 1, 256>(v, s, stream);
         else if (shape == 128) {
             if (pl == 3) launch_plane<128, 128, 2, 256>(v, s, stream);  // cluster variant (diagnostic)
