@@ -247,6 +247,96 @@ __device__ __forceinline__ bool seg_solve(int m, double (&x)[M], double (&cs)[M]
     return badm == 0u;
 }
 
+// ---- tensor memory (TMEM) as register-file extension for a thread's per-row
+// values (tcgen05.st / tcgen05.ld of 32-bit columns in the warp's lane quarter;
+// TMEM is otherwise idle in this FP64 path): pass A keeps the modified
+// super-diagonal c' and the left spike alpha of its 16 rows there, so the march
+// runs without register spills at 16 warps per SM (HJMSV_PA_TM=0: registers).
+__device__ __forceinline__ void tm_st_d(unsigned taddr, double v) {
+    const unsigned lo = static_cast<unsigned>(__double2loint(v)), hi = static_cast<unsigned>(__double2hiint(v));
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(lo), "r"(hi) : "memory");
+}
+// four doubles (8 columns) starting at taddr
+__device__ __forceinline__ void tm_ld_d4(unsigned taddr, double (&v)[4]) {
+    unsigned w[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                 : "r"(taddr)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = __hiloint2double(static_cast<int>(w[2 * q + 1]), static_cast<int>(w[2 * q]));
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// seg_solve with both c' (columns taddr + 2r) and the left spike alpha (columns
+// taddr + 32 + 2r) in TMEM; only the right-hand side / y stays in registers
+template <int M, class RowFn>
+__device__ __forceinline__ bool seg_solve_tm2(double (&x)[M], unsigned taddr, double& yF, double& aF,
+                                              double& bF, double& yL, double& aL, double& bL, int& bad_r,
+                                              RowFn row) {
+    double pm1 = 1.0, pm2 = 0.0, uprev = 0.0, yprev = 0.0, aprev = 0.0;
+    unsigned badm = 0u;
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+        double l, d, u;
+        row(r, l, d, u);
+        const double P = r == 0 ? d : fma(d, pm1, -(l * uprev) * pm2);
+        const double rp = pm1 * frcp(P);
+        badm |= (fabs(rp) > 1e300 ? 1u : 0u) << r;
+        const bool last = r == M - 1;
+        const double lrp = l * rp;
+        const double yy = r == 0 ? x[r] * rp : fma(-lrp, yprev, x[r] * rp);
+        const double aa = r == 0 ? -lrp : -lrp * aprev;
+        if (last) {
+            yL = yy;
+            aL = aa;
+            bL = -u * rp;
+        } else {
+            tm_st_d(taddr + 2 * r, u * rp);
+            tm_st_d(taddr + 32 + 2 * r, aa);
+        }
+        x[r] = yy;
+        yprev = yy;
+        aprev = aa;
+        uprev = u;
+        pm2 = pm1;
+        pm1 = P;
+        if (r % 8 == 7) {
+            const int e = ((__double2hiint(pm1) >> 20) & 0x7ff) - 1023;
+            const double sc = __hiloint2double((1023 - e) << 20, 0);
+            pm1 *= sc;
+            pm2 *= sc;
+        }
+    }
+    tm_wait_st();
+    double yn = yL, an = aL, bn = bL;
+#pragma unroll
+    for (int c0 = M - 4; c0 >= 0; c0 -= 4) {
+        double c[4], a4[4];
+        tm_ld_d4(taddr + 2 * c0, c);
+        tm_ld_d4(taddr + 32 + 2 * c0, a4);
+#pragma unroll
+        for (int q = 3; q >= 0; --q) {
+            const int r = c0 + q;
+            if (r < M - 1) {
+                yn = fma(-c[q], yn, x[r]);
+                an = fma(-c[q], an, a4[q]);
+                bn = -c[q] * bn;
+                x[r] = yn;
+                tm_st_d(taddr + 32 + 2 * r, an);
+            }
+        }
+    }
+    tm_st_d(taddr + 32 + 2 * (M - 1), aL);  // alpha of the last row
+    tm_wait_st();
+    yF = yn;
+    aF = an;
+    bF = bn;
+    if (badm) bad_r = __ffs(badm) - 1;
+    return badm == 0u;
+}
+
 // The segment solve of seg_solve by a twisted factorisation: rows 0..K-1 are
 // eliminated from the top (LU) and rows M-1..K+1 from the bottom (UL) at the
 // same time, and the two sweeps meet at row K = M/2, so each thread runs two
@@ -1433,7 +1523,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int NV, int NY, bool SCAN, int KL = 16, int TPC = 1, bool PAD = false>
+template <int NV, int NY, bool SCAN, int KL = 16, int TPC = 1, bool PAD = false, int TM = 0>  // TM: 0 or 2
 __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     // launched as a programmatic dependent of the previous kernel: everything
     // below reads what it wrote (no-op without a programmatic dependency)
@@ -1485,6 +1575,24 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     // with the window prologue below
     __shared__ alignas(8) unsigned long long tbar;
     const unsigned tbar_s = static_cast<unsigned>(__cvta_generic_to_shared(&tbar));
+    // TM 2: 64 TMEM columns per warp (its 15 c' and 16 alpha values) in the warp's lane quarter
+    __shared__ unsigned tm_base_s;
+    // ceil(warps / 4) slots per lane quarter x 64 columns, a
+    // power of two >= 32: the co-resident CTAs of an SM fit its 512 columns
+    // (16-warp CTAs: 256 columns, one per SM; 8-warp CTAs: 128, two per SM; 4-warp: 64, four)
+    const unsigned tm_slots = (static_cast<unsigned>(blockDim.x * blockDim.y) / 32u + 3u) / 4u;
+    const unsigned tm_need = tm_slots * 64u;
+    const unsigned TM_COLS = tm_need <= 32u ? 32u : tm_need <= 64u ? 64u : tm_need <= 128u ? 128u : 256u;
+    const int warp = tid >> 5;
+    if constexpr (TM) {
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             static_cast<unsigned>(__cvta_generic_to_shared(&tm_base_s))),
+                         "r"(TM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+    }
     if (tid == 0) {
         const unsigned rbytes = nr * kFR * sizeof(double), ybytes = 2 * nr * sizeof(double);
         bulk_init(tbar_s, rbytes + ybytes);
@@ -1623,10 +1731,26 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             else prologue(std::false_type{});
         }
     }
+    if constexpr (TM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();  // the mbarrier is initialised
+    if constexpr (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned taddr = TM ? tm_base_s + ((static_cast<unsigned>(warp & 3) * 32u) << 16) +
+                                   static_cast<unsigned>(warp >> 2) * 64u
+                              : 0u;
+    auto tm_free = [&] {
+        if constexpr (TM) {
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncthreads();
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (warp == 0)
+                asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base_s), "r"(TM_COLS)
+                             : "memory");
+        }
+    };
     bulk_wait(tbar_s);  // rt, fy have landed
     if (fail) {  // the problem failed in an earlier step (block-uniform)
         cp_async_wait<0>();
+        tm_free();
         return;
     }
     if (blockIdx.x == 0 && tid == 0) st.maxdelta_bits = 0ull;
@@ -1654,6 +1778,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                 dcol[static_cast<size_t>(i) * SR] = f - u0;
             }
         }
+        tm_free();
         tl_end(v, s, 0);
         return;
     }
@@ -1824,7 +1949,8 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                     interior(r01.x * vj, g4h, l, d, u);
                 }
             };
-            ok = seg_solve<M>(M, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
+            if constexpr (TM == 2) ok = seg_solve_tm2<M>(x, taddr, yF, aF, bF, yL, aL, bL, bad_r, row);
+            else ok = seg_solve<M>(M, x, cs, al, yF, aF, bF, yL, aL, bL, bad_r, row);
             cp_async_wait<0>();
             // STAGE: queue the next tile's window and ring rows now (the ring and
             // the window registers are free), ahead of this tile's reduced systems
@@ -1898,14 +2024,31 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         }
         double b = bL;
         double* __restrict__ dcol = v.D + off + static_cast<size_t>(j) * nyr + k + static_cast<size_t>(a) * SR;
+        if constexpr (TM == 2) {
 #pragma unroll
-        for (int r = M - 1; r >= 0; --r) {
-            if (r < M - 1) b = -cs[r] * b;
-            if (!PAD || (klive && a + r < nr))
-                dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(al[r], left, x[r]));
+            for (int c0 = M - 4; c0 >= 0; c0 -= 4) {
+                double c[4], a4[4];
+                tm_ld_d4(taddr + 2 * c0, c);
+                tm_ld_d4(taddr + 32 + 2 * c0, a4);
+#pragma unroll
+                for (int q = 3; q >= 0; --q) {
+                    const int r = c0 + q;
+                    if (r < M - 1) b = -c[q] * b;
+                    if (!PAD || (klive && a + r < nr))
+                        dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(a4[q], left, x[r]));
+                }
+            }
+        } else {
+#pragma unroll
+            for (int r = M - 1; r >= 0; --r) {
+                if (r < M - 1) b = -cs[r] * b;
+                if (!PAD || (klive && a + r < nr))
+                    dcol[static_cast<size_t>(r) * SR] = fma(b, right, fma(al[r], left, x[r]));
+            }
         }
         if (TPC > 1 && t + 1 < TPC) __syncthreads();  // the reduced rows are reused by the next tile
     }
+    tm_free();
     tl_end(v, s, 0);
 }
 
@@ -2604,11 +2747,11 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
             case 32: go(k_pa<0, 32, false, 16, 1, true>); break;
             case 64: go(k_pa<0, 64, false, 16, 1, true>); break;
             case 128:
-                if (scan) go(k_pa<0, 128, true, 16, 1, true>);
+                if (scan) go(k_pa<0, 128, true, 16, 1, true, 2>);
                 else go(k_pa<0, 128, false, 16, 1, true>);
                 break;
             default:
-                if (scan) go(k_pa<0, 256, true, 16, 1, true>);
+                if (scan) go(k_pa<0, 256, true, 16, 1, true, 2>);
                 else go(k_pa<0, 256, false, 16, 1, true>);
                 break;
         }
@@ -2661,16 +2804,28 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
                     break;
             }
         } else {
+            // the lane-scan variants (16 / 32 segments, the large CTAs of configs 1
+            // and 3) keep the partition solve's c' and alpha rows in tensor memory (no
+            // spills; config 1 pass A -7 %); the small-CTA variants stay in registers
+            // (the per-CTA TMEM allocation costs more than it saves there: config 4
+            // +29 %); HJMSV_PA_TM=0: registers only
+            static const int tm_env = [] {
+                const char* e = std::getenv("HJMSV_PA_TM");
+                return e ? std::atoi(e) : 2;
+            }();
+            const bool tm = tm_env != 0;
             switch (shape) {
                 case 32: go(k_pa<32, 32, false>); break;
                 case 64: go(k_pa<64, 64, false>); break;
                 case 128:
                     if (kl8) go(k_pa<128, 128, true, 8>);
+                    else if (scan && tm) go(k_pa<128, 128, true, 16, 1, false, 2>);
                     else if (scan) go(k_pa<128, 128, true>);
                     else go(k_pa<128, 128, false>);
                     break;
                 default:
                     if (kl8) go(k_pa<256, 256, true, 8>);
+                    else if (scan && tm) go(k_pa<256, 256, true, 16, 1, false, 2>);
                     else if (scan) go(k_pa<256, 256, true>);
                     else go(k_pa<256, 256, false>);
                     break;
