@@ -2818,13 +2818,15 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
                 case 32: go(k_pa<32, 32, false>); break;
                 case 64: go(k_pa<64, 64, false>); break;
                 case 128:
-                    if (kl8) go(k_pa<128, 128, true, 8>);
+                    if (kl8 && tm) go(k_pa<128, 128, true, 8, 1, false, 2>);
+                    else if (kl8) go(k_pa<128, 128, true, 8>);
                     else if (scan && tm) go(k_pa<128, 128, true, 16, 1, false, 2>);
                     else if (scan) go(k_pa<128, 128, true>);
                     else go(k_pa<128, 128, false>);
                     break;
                 default:
-                    if (kl8) go(k_pa<256, 256, true, 8>);
+                    if (kl8 && tm) go(k_pa<256, 256, true, 8, 1, false, 2>);
+                    else if (kl8) go(k_pa<256, 256, true, 8>);
                     else if (scan && tm) go(k_pa<256, 256, true, 16, 1, false, 2>);
                     else if (scan) go(k_pa<256, 256, true>);
                     else go(k_pa<256, 256, false>);
