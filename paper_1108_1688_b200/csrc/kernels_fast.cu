@@ -270,7 +270,7 @@ __device__ __forceinline__ void tm_ld_d4(unsigned taddr, double (&v)[4]) {
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // seg_solve with both c' (columns taddr + 2r) and the left spike alpha (columns
-// taddr + 32 + 2r) in TMEM; only the right-hand side / y stays in registers
+// taddr + 2M + 2r) in TMEM; only the right-hand side / y stays in registers
 template <int M, class RowFn>
 __device__ __forceinline__ bool seg_solve_tm2(double (&x)[M], unsigned taddr, double& yF, double& aF,
                                               double& bF, double& yL, double& aL, double& bL, int& bad_r,
@@ -294,7 +294,7 @@ __device__ __forceinline__ bool seg_solve_tm2(double (&x)[M], unsigned taddr, do
             bL = -u * rp;
         } else {
             tm_st_d(taddr + 2 * r, u * rp);
-            tm_st_d(taddr + 32 + 2 * r, aa);
+            tm_st_d(taddr + 2 * M + 2 * r, aa);
         }
         x[r] = yy;
         yprev = yy;
@@ -315,7 +315,7 @@ __device__ __forceinline__ bool seg_solve_tm2(double (&x)[M], unsigned taddr, do
     for (int c0 = M - 4; c0 >= 0; c0 -= 4) {
         double c[4], a4[4];
         tm_ld_d4(taddr + 2 * c0, c);
-        tm_ld_d4(taddr + 32 + 2 * c0, a4);
+        tm_ld_d4(taddr + 2 * M + 2 * c0, a4);
 #pragma unroll
         for (int q = 3; q >= 0; --q) {
             const int r = c0 + q;
@@ -324,11 +324,11 @@ __device__ __forceinline__ bool seg_solve_tm2(double (&x)[M], unsigned taddr, do
                 an = fma(-c[q], an, a4[q]);
                 bn = -c[q] * bn;
                 x[r] = yn;
-                tm_st_d(taddr + 32 + 2 * r, an);
+                tm_st_d(taddr + 2 * M + 2 * r, an);
             }
         }
     }
-    tm_st_d(taddr + 32 + 2 * (M - 1), aL);  // alpha of the last row
+    tm_st_d(taddr + 2 * M + 2 * (M - 1), aL);  // alpha of the last row
     tm_wait_st();
     yF = yn;
     aF = an;
@@ -1523,13 +1523,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int NV, int NY, bool SCAN, int KL = 16, int TPC = 1, bool PAD = false, int TM = 0>  // TM: 0 or 2
+// TM: 0 or 2; SEG: rows per r-segment (16, or 32 with the arrays in TMEM)
+template <int NV, int NY, bool SCAN, int KL = 16, int TPC = 1, bool PAD = false, int TM = 0, int SEG = 16>
 __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     // launched as a programmatic dependent of the previous kernel: everything
     // below reads what it wrote (no-op without a programmatic dependency)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     tl_begin(v, s, 0);
-    constexpr int M = 16;
+    constexpr int M = SEG;
+    static_assert(SEG == 16 || (SEG == 32 && TM == 2), "32-row segments keep their arrays in TMEM");
     // PAD: any nv, any ny <= NY and any nr <= 512 (the reference's own meshes):
     // the grid's real sizes are runtime values, k lanes past ny and rows past nr
     // run inert (identity rows, no stores); otherwise NV x NY exactly
@@ -1577,12 +1579,13 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     const unsigned tbar_s = static_cast<unsigned>(__cvta_generic_to_shared(&tbar));
     // TM 2: 64 TMEM columns per warp (its 15 c' and 16 alpha values) in the warp's lane quarter
     __shared__ unsigned tm_base_s;
-    // ceil(warps / 4) slots per lane quarter x 64 columns, a
+    // ceil(warps / 4) slots per lane quarter x 4M columns, a
     // power of two >= 32: the co-resident CTAs of an SM fit its 512 columns
     // (16-warp CTAs: 256 columns, one per SM; 8-warp CTAs: 128, two per SM; 4-warp: 64, four)
     const unsigned tm_slots = (static_cast<unsigned>(blockDim.x * blockDim.y) / 32u + 3u) / 4u;
-    const unsigned tm_need = tm_slots * 64u;
-    const unsigned TM_COLS = tm_need <= 32u ? 32u : tm_need <= 64u ? 64u : tm_need <= 128u ? 128u : 256u;
+    const unsigned tm_need = tm_slots * (4u * M);
+    const unsigned TM_COLS = tm_need <= 32u ? 32u : tm_need <= 64u ? 64u : tm_need <= 128u ? 128u
+                             : tm_need <= 256u ? 256u : 512u;
     const int warp = tid >> 5;
     if constexpr (TM) {
         if (warp == 0) {
@@ -1735,7 +1738,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     __syncthreads();  // the mbarrier is initialised
     if constexpr (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const unsigned taddr = TM ? tm_base_s + ((static_cast<unsigned>(warp & 3) * 32u) << 16) +
-                                   static_cast<unsigned>(warp >> 2) * 64u
+                                   static_cast<unsigned>(warp >> 2) * (4u * M)
                               : 0u;
     auto tm_free = [&] {
         if constexpr (TM) {
@@ -2029,7 +2032,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
             for (int c0 = M - 4; c0 >= 0; c0 -= 4) {
                 double c[4], a4[4];
                 tm_ld_d4(taddr + 2 * c0, c);
-                tm_ld_d4(taddr + 32 + 2 * c0, a4);
+                tm_ld_d4(taddr + 2 * M + 2 * c0, a4);
 #pragma unroll
                 for (int q = 3; q >= 0; --q) {
                     const int r = c0 + q;
@@ -2052,8 +2055,8 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     tl_end(v, s, 0);
 }
 
-inline size_t pa_smem(int nr, int kl = 16, int tpc = 1) {
-    const int S = (nr + 15) / 16, nt = kl * S;
+inline size_t pa_smem(int nr, int kl = 16, int tpc = 1, int seg = 16) {
+    const int S = (nr + seg - 1) / seg, nt = kl * S;
     const int rst = kRing * 4 + (tpc > 1 ? 12 : 0) + 1;
     return sizeof(double) * (static_cast<size_t>(kl) * (8 * S + 9) + static_cast<size_t>(rst) * nt +
                              static_cast<size_t>(nr) * (kFR + 2));
@@ -2754,6 +2757,39 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
                 if (scan) go(k_pa<0, 256, true, 16, 1, true, 2>);
                 else go(k_pa<0, 256, false, 16, 1, true>);
                 break;
+        }
+        mark(0, "fx_explicit_sweep_r", 16.0);
+    } else if (pa && [&] {
+                   // 32-row segments for 512-row lines (config 3: two 256-thread CTAs
+                   // per SM, half the per-segment overheads; measured 340 -> 299 us);
+                   // HJMSV_PA_SEG=16 keeps 16-row segments, 32 forces them where they fit
+                   static const int seg_env = [] {
+                       const char* e = std::getenv("HJMSV_PA_SEG");
+                       return e ? std::atoi(e) : 0;
+                   }();
+                   const bool fits = (shape == 128 || shape == 256) && v.nr % 32 == 0 &&
+                                     (v.nr / 32 == 8 || v.nr / 32 == 16) && !(v.dbg & 2);
+                   return fits && (seg_env == 32 || seg_env == 33 || (seg_env == 0 && v.nr == 512));
+               }()) {
+        // pass A fused, 32-row segments with c' and alpha in tensor memory
+        const int S = v.nr / 32;
+        const dim3 g(v.nv * (v.ny / 16), v.P), b(16, S);
+        const size_t sm = pa_smem(v.nr, 16, 1, 32);
+        auto go = [&](auto kern) {
+            smem_attr(reinterpret_cast<const void*>(kern), sm);
+            launch_pdl(kern, g, b, sm, stream, v, s);
+        };
+        static const bool seg_noscan = [] {  // HJMSV_PA_SEG=33: warp 0's two-ended recurrence
+            const char* e = std::getenv("HJMSV_PA_SEG");
+            return e && std::atoi(e) == 33;
+        }();
+        const bool scan = S == 16 && !seg_noscan;
+        if (shape == 256) {
+            if (scan) go(k_pa<256, 256, true, 16, 1, false, 2, 32>);
+            else go(k_pa<256, 256, false, 16, 1, false, 2, 32>);
+        } else {
+            if (scan) go(k_pa<128, 128, true, 16, 1, false, 2, 32>);
+            else go(k_pa<128, 128, false, 16, 1, false, 2, 32>);
         }
         mark(0, "fx_explicit_sweep_r", 16.0);
     } else if (pa) {
