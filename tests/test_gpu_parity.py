@@ -500,3 +500,15 @@ def test_padded_pass_a_shapes(gpu, oracle, shape):
         s.run()
         g, price = s.grid(0), float(s.spot_prices()[0])
     assert_parity(p, g, price, oracle, "fast")
+
+
+def test_pass_a_32_row_segments(gpu, oracle):
+    """512-row lines run pass A with 32-row segments whose c' and alpha rows live
+    in tensor memory (16 segments, lane-scan reduced systems); on a 128-wide plane
+    too, against the oracle."""
+    p = W.make_problem(2, 8, nr=512, nv=128, ny=128, steps=6)
+    with hj.Solver([p], mode="fast") as s:
+        s.step(6)
+        g = s.grid(0)
+    g_ref = oracle.run(p, steps=6)[0]
+    assert B.normwise_rel(g, g_ref) <= TOL
