@@ -268,6 +268,25 @@ __device__ __forceinline__ void tm_ld_d4(unsigned taddr, double (&v)[4]) {
     for (int q = 0; q < 4; ++q) v[q] = __hiloint2double(static_cast<int>(w[2 * q + 1]), static_cast<int>(w[2 * q]));
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// two 4-double loads under one wait::ld
+__device__ __forceinline__ void tm_ld_d4x2(unsigned ta, double (&va)[4], unsigned tb, double (&vb)[4]) {
+    unsigned w[16];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                 : "r"(ta)
+                 : "memory");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]),
+                   "=r"(w[15])
+                 : "r"(tb)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        va[q] = __hiloint2double(static_cast<int>(w[2 * q + 1]), static_cast<int>(w[2 * q]));
+        vb[q] = __hiloint2double(static_cast<int>(w[8 + 2 * q + 1]), static_cast<int>(w[8 + 2 * q]));
+    }
+}
 
 // seg_solve with both c' (columns taddr + 2r) and the left spike alpha (columns
 // taddr + 2M + 2r) in TMEM; only the right-hand side / y stays in registers
@@ -314,8 +333,7 @@ __device__ __forceinline__ bool seg_solve_tm2(double (&x)[M], unsigned taddr, do
 #pragma unroll
     for (int c0 = M - 4; c0 >= 0; c0 -= 4) {
         double c[4], a4[4];
-        tm_ld_d4(taddr + 2 * c0, c);
-        tm_ld_d4(taddr + 2 * M + 2 * c0, a4);
+        tm_ld_d4x2(taddr + 2 * c0, c, taddr + 2 * M + 2 * c0, a4);
 #pragma unroll
         for (int q = 3; q >= 0; --q) {
             const int r = c0 + q;
@@ -2031,8 +2049,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
 #pragma unroll
             for (int c0 = M - 4; c0 >= 0; c0 -= 4) {
                 double c[4], a4[4];
-                tm_ld_d4(taddr + 2 * c0, c);
-                tm_ld_d4(taddr + 2 * M + 2 * c0, a4);
+                tm_ld_d4x2(taddr + 2 * c0, c, taddr + 2 * M + 2 * c0, a4);
 #pragma unroll
                 for (int q = 3; q >= 0; --q) {
                     const int r = c0 + q;
