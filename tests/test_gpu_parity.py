@@ -512,3 +512,21 @@ def test_pass_a_32_row_segments(gpu, oracle):
         g = s.grid(0)
     g_ref = oracle.run(p, steps=6)[0]
     assert B.normwise_rel(g, g_ref) <= TOL
+
+
+def test_concurrent_handles_tensor_memory_and_model_functions(gpu, oracle):
+    """Two handles at once on one device (hjmsv_batch_run over devices [0, 0]): their
+    pass-A CTAs share the SMs' tensor memory (the lane-scan variants allocate TMEM
+    columns per CTA), half the problems carry model functions of t; every grid
+    against the oracle."""
+    probs = [W.make_problem(1, q, steps=6) for q in range(4)]
+    probs[1] = W.with_model_functions(probs[1])
+    probs[2] = W.with_model_functions(probs[2], amp=-0.25)
+    prices, reps, grids = hj.batch_run(probs, devices=[0, 0], mode="fast", grids=True)
+    off = 0
+    for q, p in enumerate(probs):
+        assert reps[q]["status"] == 0 and reps[q]["steps_done"] == 6
+        g = grids[off:off + p.size].reshape(p.shape)
+        off += p.size
+        g_ref = oracle.run(p)[0]
+        assert B.normwise_rel(g, g_ref) <= TOL, q
