@@ -2650,11 +2650,16 @@ void launch_pdl(K kernel, dim3 g, dim3 b, size_t sm, cudaStream_t stream, const 
 template <int NV, int NY, int CS, int NT, int MB = 0, bool PAD = false>
 void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
     using G = PlaneGeom<NV, NY, CS, NT, MB>;
-    smem_attr(reinterpret_cast<const void*>(k_plane<NV, NY, CS, NT, MB, PAD>), G::SMEM);
+    // HJMSV_PB_PAD (diagnostic): extra dynamic shared memory, to pin fewer CTAs per SM
+    static const size_t pb_pad = [] {
+        const char* e = std::getenv("HJMSV_PB_PAD");
+        return e ? static_cast<size_t>(std::atoll(e)) : size_t(0);
+    }();
+    smem_attr(reinterpret_cast<const void*>(k_plane<NV, NY, CS, NT, MB, PAD>), G::SMEM + pb_pad);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(v.nr * v.P * CS);
     cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = G::SMEM;
+    cfg.dynamicSmemBytes = G::SMEM + pb_pad;
     cfg.stream = stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
