@@ -2395,7 +2395,9 @@ k_plane(BatchView v, int s) {
         // chunks (lane l holds elements 64q + 2l) and are exchanged with the
         // lanes that own them through the warp's tile rows, which are free once
         // every lane has read its x; loads are in flight through the solve
-        constexpr bool early_u = G::MINB == 1;       // registers for U in flight through the solve
+        // registers for U in flight through the solve (one 8-warp CTA per SM; the
+        // 16-warp variant keeps its 128 registers for the solve instead)
+        constexpr bool early_u = G::MINB == 1 && NT <= 256;
         constexpr int WROWS = 32 / LY;
         constexpr bool stage_u = WROWS * NY == 512 && ALL_LIVE && !PAD;  // all benchmarked shapes
         const int jw = jl & ~(WROWS - 1);  // the warp's first row
@@ -2418,25 +2420,38 @@ k_plane(BatchView v, int s) {
         double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
         if (solve && !(v.dbg & 4)) {
             const double h1 = a_i * vtab[5 * NV + j];
-            double lr[MS];  // th g6 / (2 dxy) per row
+            // th g6 / (2 dxy) per row: a table (8-warp CTAs) or recomputed at each use
+            // (16-warp CTAs, whose 128 registers hold the solve's arrays)
+            constexpr bool LR_TAB = NT <= 256;
+            double lr[LR_TAB ? MS : 1];
+            auto lrv = [&](int r) {
+                if constexpr (LR_TAB) {
+                    return lr[r];
+                } else {
+                    const double2 st6 = reinterpret_cast<const double2*>(ytab)[sy * 17 + r];
+                    return fma(h1, st6.x, st6.y);
+                }
+            };
+            if constexpr (LR_TAB) {
 #pragma unroll
-            for (int r = 0; r < MS; ++r) {
-                const double2 st6 = reinterpret_cast<const double2*>(ytab)[sy * 17 + r];
-                lr[r] = fma(h1, st6.x, st6.y);
+                for (int r = 0; r < MS; ++r) {
+                    const double2 st6 = reinterpret_cast<const double2*>(ytab)[sy * 17 + r];
+                    lr[r] = fma(h1, st6.x, st6.y);
+                }
             }
-            double f0d = dint, f0u = -lr[0];
+            double f0d = dint, f0u = -lrv(0);
             if (sy == 0) {  // row 0 (discretization.cpp:274-289), folded (solver.cpp:28-40)
                 f0d = 1.0;
                 f0u = 0.0;
                 if (!yminD) {
                     if (v.y_order == 1) {
-                        f0d = fma(2.0, lr[0], fma(th, react, 1.0));
-                        f0u = -2.0 * lr[0];
+                        f0d = fma(2.0, lrv(0), fma(th, react, 1.0));
+                        f0u = -2.0 * lrv(0);
                     } else {
-                        f0d = fma(3.0, lr[0], fma(th, react, 1.0));
-                        f0u = -4.0 * lr[0];
-                        const double s20 = lr[0];
-                        const double l1 = lr[1], u1 = -lr[1];
+                        f0d = fma(3.0, lrv(0), fma(th, react, 1.0));
+                        f0u = -4.0 * lrv(0);
+                        const double s20 = lrv(0);
+                        const double l1 = lrv(1), u1 = -lrv(1);
                         if (fabs(u1) > 1e-300) {
                             const double f = s20 / u1;
                             f0d = fma(-f, l1, f0d);
@@ -2455,7 +2470,8 @@ k_plane(BatchView v, int s) {
                 } else if (PAD ? (a + r >= nyr - 1 && (a + r > nyr - 1 || ymaxD)) : (r == MS - 1 && lastI)) {
                     l = 0.0; d = 1.0; u = 0.0;  // the y_max face row (PAD: and the inert rows past it)
                 } else {
-                    l = lr[r]; d = dint; u = -lr[r];
+                    const double q = lrv(r);
+                    l = q; d = dint; u = -q;
                 }
             };
             int bad_r = 0;
@@ -2915,11 +2931,14 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         else if (shape == 32) launch_plane<32, 32, 1, 64>(v, s, stream);
         else if (shape == 64) launch_plane<64, 64, 1, 256>(v, s, stream);
         else if (shape == 128) {
-            if (pl == 3) launch_plane<128, 128, 2, 256>(v, s, stream);  // cluster variant (diagnostic)
-            else if (pl == 4) launch_plane<128, 128, 1, 512>(v, s, stream);  // 16 warps (diagnostic)
-            else launch_plane<128, 128, 1, 256>(v, s, stream);
-        } else if (pl == 4) launch_plane<256, 256, 4, 512>(v, s, stream);
-        else launch_plane<256, 256, 4, 256>(v, s, stream);
+            // 16 warps (512 threads at 128 registers: the y-row coefficients recomputed
+            // at each use, U loaded after the solve) — measured faster than 8 warps at
+            // 243 registers; HJMSV_PLANE=2: the 8-warp plane; 3: 2-CTA clusters (diagnostics)
+            if (pl == 3) launch_plane<128, 128, 2, 256>(v, s, stream);
+            else if (pl == 2) launch_plane<128, 128, 1, 256>(v, s, stream);
+            else launch_plane<128, 128, 1, 512>(v, s, stream);
+        } else if (pl == 2) launch_plane<256, 256, 4, 256>(v, s, stream);
+        else launch_plane<256, 256, 4, 512>(v, s, stream);
         mark(2, "fx_plane_vy_update", 24.0);
         return;
     }

@@ -411,7 +411,8 @@ print("WORST", worst)
 
 
 @pytest.mark.parametrize("env", [{"HJMSV_PLANE": "0"}, {"HJMSV_PLANE": "0", "HJMSV_PA": "0"},
-                                 {"HJMSV_PLANE": "3"}, {"HJMSV_DBG": "2"}])
+                                 {"HJMSV_PLANE": "3"}, {"HJMSV_PLANE": "2"}, {"HJMSV_DBG": "2"},
+                                 {"HJMSV_PA_TM": "0", "HJMSV_PA_SEG": "16"}])
 def test_diagnostic_schedules(gpu, env):
     """The schedules behind the diagnostic switches (split v + y kernels with the
     lane-scan k_y3, the four-kernel schedule, the 2-CTA cluster plane, pass A's
