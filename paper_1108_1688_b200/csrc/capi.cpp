@@ -234,6 +234,7 @@ struct hjmsv_solver {
     double *U = nullptr, *D = nullptr, *C = nullptr, *U0 = nullptr;
     double *axes = nullptr, *steps = nullptr, *fast = nullptr, *fb = nullptr;
     double* ab = nullptr;      // per-step a_i, b_i (model functions of t only)
+    double* ylu = nullptr;     // y-line pivot table of pass B (constant models, two-pass shapes)
     ProblemConst* pc = nullptr;
     DevStatus* st = nullptr;
     long long* spot_idx = nullptr;
@@ -256,7 +257,7 @@ struct hjmsv_solver {
         if (stream) cudaStreamSynchronize(stream);  // buffers return to the pool only when idle
         if (graph) cudaGraphExecDestroy(graph);
         for (void* p : {(void*)U, (void*)D, (void*)C, (void*)U0, (void*)axes, (void*)steps,
-                        (void*)fast, (void*)fb, (void*)ab, (void*)pc, (void*)st, (void*)spot_idx, (void*)spot_w,
+                        (void*)fast, (void*)fb, (void*)ab, (void*)ylu, (void*)pc, (void*)st, (void*)spot_idx, (void*)spot_w,
                         (void*)spot_out})
             dfree(p);
         if (ev0) cudaEventDestroy(ev0);
@@ -559,6 +560,28 @@ hjmsv_solver* create_handle(const hjmsv_problem* problems, int count,
         CK(cudaMemcpyAsync(h->fast, fast_h, sizeof(double) * fast_n, cudaMemcpyHostToDevice, h->stream));
         CK(cudaStreamSynchronize(h->stream));
         pt.mark("fast tables");
+        // constant models: the y-line matrices are the same at every step, so their
+        // pivots (the reference's Thomas order) are computed once; a vanishing or
+        // non-finite pivot keeps the handle on the partition method, which reports it
+        if (fast_ylu_supported(v)) {
+            h->ylu = dalloc<double>(PN);
+            int* flag = dalloc<int>(count);
+            CK(cudaMemsetAsync(flag, 0, sizeof(int) * count, h->stream));
+            fast_ylu_build(v, h->ylu, flag, h->stream);
+            std::vector<int> fl(count);
+            CK(cudaMemcpyAsync(fl.data(), flag, sizeof(int) * count, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            dfree(flag);
+            bool ok = true;
+            for (int f : fl) ok = ok && f == 0;
+            if (ok) {
+                v.ylu = h->ylu;
+            } else {
+                dfree(h->ylu);
+                h->ylu = nullptr;
+            }
+            pt.mark("y-line pivots");
+        }
     }
     if (init_mode == INIT_DEVICE) {
         TermParam* tp = dalloc<TermParam>(count);

@@ -81,6 +81,10 @@ struct BatchView {
     // the earliest block start and the latest block end in %globaltimer ns, so
     // per-kernel durations are taken in the launch mode of the timed march
     unsigned long long* tl;
+    // y-line LU of a constant model (the y-line matrices do not change between
+    // steps): 1 / pivot of the reference's Thomas elimination (solver.cpp:42-50)
+    // per node, [P][N] in pass B's warp-block order (fast_ylu_build), or null
+    const double* ylu;
 };
 constexpr int kTlSlots = 5;  // 0 pass A / explicit, 1 r-lines, 2 pass B / v-lines, 3 y-lines, 4 faces
 
@@ -138,6 +142,11 @@ void fast_step(const BatchView& v, int s, cudaStream_t stream, long long* launch
 void strict_explicit(const BatchView& v, int s, cudaStream_t stream);
 void fast_explicit(const BatchView& v, int s, cudaStream_t stream);
 int fast_stride(int nr, int nv, int ny);
+// y-line pivots of a constant-model batch for pass B (exact two-pass shapes only):
+// fills ylu [P][N] and sets flag[p] != 0 where a pivot vanished or left the
+// finite range; false when the shape has no table-driven pass B
+bool fast_ylu_supported(const BatchView& v);
+void fast_ylu_build(const BatchView& v, double* ylu, int* flag, cudaStream_t stream);
 bool fast_supported(int nr, int nv, int ny);
 void reset_status(const BatchView& v, cudaStream_t stream);
 // Monte Carlo validator (kernels_mc.cu): run_path's constants (montecarlo.cpp:38-79)

@@ -2125,7 +2125,45 @@ struct PlaneGeom {
     __device__ static int ci(int t, int k) { return t * CP + k; }
 };
 
-template <int NV, int NY, int CS, int NTX, int MB, bool PAD = false>
+// Row 0 of a y-line (discretization.cpp:274-289) with its second super-diagonal
+// folded into row 1 (solver.cpp:28-40): the row's diagonal f0d and upper f0u, and
+// what the fold does to the right-hand side: x0 -= f x1 (f != 0), or the lagged
+// x0 -= s20 x2 when row 1's upper coupling vanishes (lag). q0, q1 = theta dt
+// g6 / (2 dxy) of rows 0 and 1. Shared by pass B and the pivot table build.
+struct YRow0 {
+    double d, u, f, s20;
+    bool lag;
+};
+__device__ __forceinline__ YRow0 y_row0(bool yminD, int y_order, double q0, double q1, double th,
+                                        double react, double dint) {
+    YRow0 o{1.0, 0.0, 0.0, 0.0, false};
+    if (yminD) return o;
+    if (y_order == 1) {
+        o.d = fma(2.0, q0, fma(th, react, 1.0));
+        o.u = -2.0 * q0;
+        return o;
+    }
+    o.d = fma(3.0, q0, fma(th, react, 1.0));
+    o.u = -4.0 * q0;
+    o.s20 = q0;
+    const double l1 = q1, u1 = -q1;
+    if (fabs(u1) > 1e-300) {
+        o.f = o.s20 / u1;
+        o.d = fma(-o.f, l1, o.d);
+        o.u = fma(-o.f, dint, o.u);
+    } else {
+        o.lag = true;
+    }
+    return o;
+}
+
+// YLU: the y-lines of a constant model are solved from the precomputed pivots
+// of the reference's own Thomas order (v.ylu, 1 / pivot per node): the forward
+// and backward substitutions are affine recurrences with known coefficients,
+// run as 16-row segment scans per lane with the segment carries resolved by two
+// lane scans per line — one right-hand side and two arrays per thread instead of
+// the partition method's three right-hand sides and per-step factorisation.
+template <int NV, int NY, int CS, int NTX, int MB, bool PAD = false, bool YLU = false>
 __global__ void __launch_bounds__(NTX, (PlaneGeom<NV, NY, CS, NTX, MB>::MINB))
 k_plane(BatchView v, int s) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of pass A
@@ -2186,6 +2224,8 @@ k_plane(BatchView v, int s) {
         if (!PAD && tid == 0) {  // U rows -> L2 early, so the update's loads hit L2
             constexpr unsigned bytes = RV * NY * sizeof(double);
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.U + pb), "r"(bytes) : "memory");
+            if constexpr (YLU)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.ylu + pb), "r"(bytes) : "memory");
         }
         if constexpr (REGV) {
             // column segments of dU1 straight into registers (lanes = k: coalesced rows)
@@ -2410,6 +2450,18 @@ k_plane(BatchView v, int s) {
         };
         if constexpr (stage_u && early_u) load_us();
         double x[MS], cs[MS], al[MS];
+        static_assert(!YLU || (stage_u && LY > 1), "table-driven y-lines: the exact two-pass shapes");
+        if constexpr (YLU) {
+            // this lane's 16 reciprocal pivots: the warp's block of the table moves
+            // as coalesced 128-bit chunks (lane l, chunk q = rows 2q, 2q+1 of its segment)
+            const double2* gq = reinterpret_cast<const double2*>(v.ylu + pb + static_cast<size_t>(jw) * NY);
+#pragma unroll
+            for (int q = 0; q < MS / 2; ++q) {
+                const double2 t2 = __ldg(gq + q * 32 + ln);
+                cs[2 * q] = t2.x;
+                cs[2 * q + 1] = t2.y;
+            }
+        }
 #pragma unroll
         for (int q = 0; q < MS / 2; ++q) {
             const double2 t2 = live ? *reinterpret_cast<const double2*>(tile + G::at(jl, a + 2 * q))
@@ -2418,6 +2470,90 @@ k_plane(BatchView v, int s) {
             x[2 * q + 1] = t2.y;
         }
         double yF = 0.0, aF = 0.0, bF = 0.0, yL = 0.0, aL = 0.0, bL = 0.0;
+        double left = 0.0, right = 0.0;
+        if constexpr (YLU) {
+            constexpr unsigned FULL = 0xffffffffu;
+            // forward substitution x'_k = (x_k - l_k x'_{k-1}) / piv_k inside the
+            // segment from a zero carry; fa = the carry's multiplier at the last row
+            double fa = 0.0, fb = 0.0;
+            if (solve) {
+                const double h1 = a_i * vtab[5 * NV + j];
+                auto lrv = [&](int r) {
+                    const double2 st6 = reinterpret_cast<const double2*>(ytab)[sy * 17 + r];
+                    return fma(h1, st6.x, st6.y);
+                };
+                double u0f = 0.0;
+                if (sy == 0) {  // row 0, folded; its pivot is in the table
+                    const YRow0 r0 = y_row0(yminD, v.y_order, lrv(0), lrv(1), th, react, dint);
+                    u0f = r0.u;
+                    if (r0.lag) x[0] = fma(-r0.s20, x[2], x[0]);
+                    else x[0] = fma(-r0.f, x[1], x[0]);
+                }
+                const bool lastI = sy == LY - 1 && ymaxD;
+                double xp = 0.0;
+                fa = 1.0;
+#pragma unroll
+                for (int r = 0; r < MS; ++r) {
+                    const double rp = cs[r];
+                    double lrp = lrv(r) * rp;  // l / piv; u = -l on interior rows: c' = -l / piv
+                    double cp = -lrp;
+                    if (r == 0 && sy == 0) {
+                        lrp = 0.0;
+                        cp = u0f * rp;
+                    }
+                    if (r == MS - 1 && lastI) lrp = cp = 0.0;  // the y_max face row
+                    xp = fma(-lrp, xp, x[r] * rp);
+                    x[r] = xp;
+                    fa *= -lrp;
+                    cs[r] = cp;
+                }
+                fb = xp;
+            }
+            // x'_last of every segment: inclusive scan of the affine maps over the line's lanes
+#pragma unroll
+            for (int off = 1; off < LY; off <<= 1) {
+                const double pa = __shfl_up_sync(FULL, fa, off, LY);
+                const double pb2 = __shfl_up_sync(FULL, fb, off, LY);
+                if (sy >= off) {
+                    fb = fma(fa, pb2, fb);
+                    fa *= pa;
+                }
+            }
+            double cin = __shfl_up_sync(FULL, fb, 1, LY);
+            if (sy == 0) cin = 0.0;
+            // carry into the rows (the multiplier of row r is the product of -l/piv
+            // up to r: c' on the rows that take a carry), then the backward
+            // substitution x_k = x'_k - c'_k x_{k+1} from a zero carry
+            double ba = 0.0, bb = 0.0;
+            if (solve) {
+                double m = cin;
+#pragma unroll
+                for (int r = 0; r < MS; ++r) {
+                    m *= cs[r];
+                    x[r] += m;
+                }
+                double xn = 0.0;
+                ba = 1.0;
+#pragma unroll
+                for (int r = MS - 1; r >= 0; --r) {
+                    xn = fma(-cs[r], xn, x[r]);
+                    x[r] = xn;
+                    ba *= -cs[r];
+                }
+                bb = xn;
+            }
+#pragma unroll
+            for (int off = 1; off < LY; off <<= 1) {  // x_first of every segment: suffix scan
+                const double na = __shfl_down_sync(FULL, ba, off, LY);
+                const double nb = __shfl_down_sync(FULL, bb, off, LY);
+                if (sy + off < LY) {
+                    bb = fma(ba, nb, bb);
+                    ba *= na;
+                }
+            }
+            right = __shfl_down_sync(FULL, bb, 1, LY);  // x_{a+16}; its multipliers are applied below
+            if (sy == LY - 1 || !solve) right = 0.0;
+        } else
         if (solve && !(v.dbg & 4)) {
             const double h1 = a_i * vtab[5 * NV + j];
             // th g6 / (2 dxy) per row: a table (8-warp CTAs) or recomputed at each use
@@ -2486,7 +2622,8 @@ k_plane(BatchView v, int s) {
         }
         // the line's reduced system: its LY segments are LY consecutive lanes of
         // one warp, solved by a lane scan (shuffles only)
-        double left = 0.0, right = 0.0;
+        if constexpr (YLU) {
+        } else
         if constexpr (LY > 1 && LY < 8) {
             // short systems: one lane per line through shared memory (measured
             // faster than the scan for 2 and 4 segments), rows as
@@ -2538,12 +2675,18 @@ k_plane(BatchView v, int s) {
             } else {
                 load_u();
             }
-            double b = bL;  // 0 on lines that are not solved, as are cs, al, left, right
+            double b = YLU ? right : bL;  // 0 on lines that are not solved, as are cs, al, left, right
 #pragma unroll
             for (int r = MS - 1; r >= 0; --r) {
+                double dq;
+                if constexpr (YLU) {  // the right carry times the product of -c' down to row r
+                    b *= -cs[r];
+                    dq = x[r] + b;
+                } else {
                 if constexpr (G::MINB == 1) b = cs[r];  // the twisted solve left beta itself
                 else if (r < MS - 1) b = -cs[r] * b;
-                const double dq = fma(b, right, fma(al[r], left, x[r]));
+                dq = fma(b, right, fma(al[r], left, x[r]));
+                }
                 un[r] += dq;
                 x[r] = dq;
             }
@@ -2663,7 +2806,58 @@ void launch_pdl(K kernel, dim3 g, dim3 b, size_t sm, cudaStream_t stream, const 
     cudaLaunchKernelEx(&cfg, kernel, v, s);
 }
 
-template <int NV, int NY, int CS, int NT, int MB = 0, bool PAD = false>
+// The pivots of every y-line of a constant-model batch in the reference's Thomas
+// order (solver.cpp:42-50: piv_k = d_k - l_k c'_{k-1}, c'_k = u_k / piv_k), row 0
+// folded (solver.cpp:28-40), the y_max face row an identity row; rows as pass B
+// builds them (discretization.cpp:261-300). One thread per line (i, j); 1 / piv
+// of node (i, j, k) goes to the slot pass B's lane reads it from: block of
+// 32/LY lines, lane = (j mod 32/LY) LY + k/16, chunk (k mod 16)/2.
+template <int NY>
+__global__ void __launch_bounds__(128) k_ylu(BatchView v, double* out, int* flag) {
+    constexpr int MS = 16, LY = NY / MS, WROWS = 32 / LY;
+    static_assert(WROWS * NY == 512, "a warp's block of the table is 512 nodes");
+    const int p = blockIdx.y;
+    const int line = blockIdx.x * blockDim.x + threadIdx.x;
+    if (line >= v.nr * v.nv) return;
+    const int i = line / v.nv, j = line - i * v.nv;
+    const FT F = ftab(v, p, 0);
+    const double th = v.pc[p].theta_dt;
+    const double a_i = F.R[kFR * i + FR_A], react = F.R[kFR * i + FR_REACT];
+    const double dint = fma(th, react, 1.0);
+    const double h1 = a_i * F.V[kFV * j + FV_V];
+    const bool yminD = dir(v, F_YMIN), ymaxD = dir(v, F_YMAX);
+    const bool planeD = (i == v.nr - 1 && dir(v, F_RMAX)) || (i == 0 && dir(v, F_RMIN));
+    const bool solve = !planeD && !((j == 0 && dir(v, F_VMIN)) || (j == v.nv - 1 && dir(v, F_VMAX)));
+    double* blk = out + static_cast<size_t>(p) * v.N + static_cast<size_t>(i) * v.nv * NY +
+                  static_cast<size_t>(j / WROWS) * (WROWS * NY);
+    const int lb = (j % WROWS) * LY;
+    auto q_of = [&](int k) { return fma(h1, th * F.Y[kFY * k + FY_S6], th * F.Y[kFY * k + FY_T6]); };
+    const YRow0 r0 = y_row0(yminD, v.y_order, q_of(0), q_of(1), th, react, dint);
+    double cprev = 0.0;
+    bool bad = false;
+#pragma unroll 4
+    for (int k = 0; k < NY; ++k) {
+        double l, d, u;
+        if (k == 0) {
+            l = 0.0; d = r0.d; u = r0.u;
+        } else if (k == NY - 1 && ymaxD) {
+            l = 0.0; d = 1.0; u = 0.0;
+        } else {
+            const double q = q_of(k);
+            l = q; d = dint; u = -q;
+        }
+        const double piv = k == 0 ? d : fma(-l, cprev, d);
+        double rp = 1.0 / piv;
+        if (!(fabs(piv) >= 1e-300) || !(fabs(rp) <= 1e300)) bad = true;  // solver.cpp:44
+        cprev = u * rp;
+        if (!solve) rp = 1.0;  // identity lines are not solved (solver.cpp:149)
+        const int sy = k >> 4, r = k & 15;
+        blk[((r >> 1) * 32 + lb + sy) * 2 + (r & 1)] = rp;
+    }
+    if (bad && solve) atomicOr(flag + p, 1);
+}
+
+template <int NV, int NY, int CS, int NT, int MB = 0, bool PAD = false, bool YLU = false>
 void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
     using G = PlaneGeom<NV, NY, CS, NT, MB>;
     // HJMSV_PB_PAD (diagnostic): extra dynamic shared memory, to pin fewer CTAs per SM
@@ -2671,7 +2865,7 @@ void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
         const char* e = std::getenv("HJMSV_PB_PAD");
         return e ? static_cast<size_t>(std::atoll(e)) : size_t(0);
     }();
-    smem_attr(reinterpret_cast<const void*>(k_plane<NV, NY, CS, NT, MB, PAD>), G::SMEM + pb_pad);
+    smem_attr(reinterpret_cast<const void*>(k_plane<NV, NY, CS, NT, MB, PAD, YLU>), G::SMEM + pb_pad);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(v.nr * v.P * CS);
     cfg.blockDim = dim3(NT);
@@ -2686,7 +2880,7 @@ void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
     at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    cudaLaunchKernelEx(&cfg, k_plane<NV, NY, CS, NT, MB, PAD>, v, s);
+    cudaLaunchKernelEx(&cfg, k_plane<NV, NY, CS, NT, MB, PAD, YLU>, v, s);
 }
 
 int plane_kernels() {
@@ -2714,6 +2908,27 @@ bool fast_supported(int nr, int nv, int ny) {
 }
 
 int fast_stride(int nr, int nv, int ny) { return fast_table_stride(nr, nv, ny); }
+
+// pass B reads the y-line pivots from a table on the exact two-pass shapes
+// (HJMSV_YLU=0: the partition method on every handle, as with model functions of t)
+bool fast_ylu_supported(const BatchView& v) {
+    static const int on = [] {
+        const char* e = std::getenv("HJMSV_YLU");
+        return e ? std::atoi(e) : 1;
+    }();
+    return on && plane_kernels() == 1 && specialised_shape(v) != 0 && v.fast_step == 0;
+}
+
+void fast_ylu_build(const BatchView& v, double* ylu, int* flag, cudaStream_t stream) {
+    const dim3 g((v.nr * v.nv + 127) / 128, v.P), b(128);
+    switch (specialised_shape(v)) {
+        case 32: k_ylu<32><<<g, b, 0, stream>>>(v, ylu, flag); break;
+        case 64: k_ylu<64><<<g, b, 0, stream>>>(v, ylu, flag); break;
+        case 128: k_ylu<128><<<g, b, 0, stream>>>(v, ylu, flag); break;
+        case 256: k_ylu<256><<<g, b, 0, stream>>>(v, ylu, flag); break;
+        default: break;
+    }
+}
 
 
 void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launches,
@@ -2928,6 +3143,10 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
         if (plane_pad == 32) launch_plane<32, 32, 1, 64, 0, true>(v, s, stream);
         else if (plane_pad == 64) launch_plane<64, 64, 1, 256, 0, true>(v, s, stream);
         else if (plane_pad == 128) launch_plane<128, 128, 1, 256, 0, true>(v, s, stream);
+        else if (v.ylu && pl == 1 && shape == 32) launch_plane<32, 32, 1, 64, 0, false, true>(v, s, stream);
+        else if (v.ylu && pl == 1 && shape == 64) launch_plane<64, 64, 1, 256, 0, false, true>(v, s, stream);
+        else if (v.ylu && pl == 1 && shape == 128) launch_plane<128, 128, 1, 512, 0, false, true>(v, s, stream);
+        else if (v.ylu && pl == 1 && shape == 256) launch_plane<256, 256, 4, 512, 0, false, true>(v, s, stream);
         else if (shape == 32) launch_plane<32, 32, 1, 64>(v, s, stream);
         else if (shape == 64) launch_plane<64, 64, 1, 256>(v, s, stream);
         else if (shape == 128) {
