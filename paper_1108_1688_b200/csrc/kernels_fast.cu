@@ -2219,6 +2219,11 @@ k_plane(BatchView v, int s) {
     constexpr int SSTEP = REGV ? NT / NY : 1;
     static_assert(!REGV || (NT % NY == 0 && (NY * SVL) % NT == 0), "register v-phase shape");
     const int kc = tid % NY, sl0 = tid / NY;
+    // two segments per thread (the 128- and 256-wide planes): the thread takes two
+    // adjacent columns of ONE segment instead, so every table value read from
+    // shared memory serves two columns and rows move as 128-bit accesses
+    constexpr bool VPAIR = REGV && !PAD && TPT == 2 && NT / (NY / 2) == SVL;
+    const int kp = tid % (NY / 2), slp = tid / (NY / 2);
     double xv[TPT][MS];
     {  // staged even for a failed problem: the loads need not wait for the status word
         if (!PAD && tid == 0) {  // U rows -> L2 early, so the update's loads hit L2
@@ -2227,7 +2232,16 @@ k_plane(BatchView v, int s) {
             if constexpr (YLU)
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.ylu + pb), "r"(bytes) : "memory");
         }
-        if constexpr (REGV) {
+        if constexpr (VPAIR) {
+            // two adjacent columns of one 16-row segment per thread: 128-bit row loads
+            const double2* src = reinterpret_cast<const double2*>(v.D + pb + static_cast<size_t>(slp) * MS * NY) + kp;
+#pragma unroll
+            for (int r = 0; r < MS; ++r) {
+                const double2 t2 = __ldg(src + static_cast<size_t>(r) * (NY / 2));
+                xv[0][r] = t2.x;
+                xv[1][r] = t2.y;
+            }
+        } else if constexpr (REGV) {
             // column segments of dU1 straight into registers (lanes = k: coalesced rows)
 #pragma unroll
             for (int q = 0; q < TPT; ++q)
@@ -2290,7 +2304,100 @@ k_plane(BatchView v, int s) {
     const bool vwork = live_p && !planeD;
 
     // ---- v-lines (columns k), skip columns on y Dirichlet faces (solver.cpp:142)
-    if constexpr (REGV) {
+    if constexpr (VPAIR) {
+        // the table LU's two substitutions as segment scans in registers, columns
+        // 2kp and 2kp+1 of local segment slp; segment end values go to every CTA of
+        // the cluster, and each thread runs the carry chain up to its own segment
+        const int g = c * SVL + slp;       // this thread's segment of the column (warp-uniform)
+        const int ag = g * MS;             // its first row
+        const bool vsa = vwork && !(kp == 0 && yminD);
+        const bool vsb = vwork && !(kp == NY / 2 - 1 && ymaxD);
+        auto bcast2 = [&](int idx, double va, double vb) {
+            if constexpr (CS > 1) {
+#pragma unroll
+                for (int r = 0; r < CS; ++r)
+                    *reinterpret_cast<double2*>(cg::this_cluster().map_shared_rank(car, r) + idx) = make_double2(va, vb);
+            } else {
+                *reinterpret_cast<double2*>(car + idx) = make_double2(va, vb);
+            }
+        };
+        if (vwork) {
+            int bad = -1;  // first singular v pivot (table NaN), warp-uniform
+#pragma unroll
+            for (int jj = 0; jj < NV; jj += 32) {
+                const unsigned m = __ballot_sync(0xffffffffu, isnan(vtab[jj + (tid & 31)]));
+                if (m && bad < 0) bad = jj + __ffs(m) - 1;
+            }
+            if (bad >= 0 && c == 0 && slp == 0) {
+                if (vsa) record_pivot(st, s, 1, i * nyr + 2 * kp, bad);
+                if (vsb) record_pivot(st, s, 1, i * nyr + 2 * kp + 1, bad);
+            }
+            double la = 0.0, lb = 0.0;
+#pragma unroll
+            for (int r = 0; r < MS; ++r) {
+                const double bq = vtab[NV + ag + r], rq = vtab[ag + r];
+                la = fma(bq, la, rq * xv[0][r]);
+                lb = fma(bq, lb, rq * xv[1][r]);
+                xv[0][r] = la;
+                xv[1][r] = lb;
+            }
+            bcast2(G::ci(g, 2 * kp), la, lb);
+        }
+        cluster_sync();
+        if (vwork) {
+            double ca = 0.0, cb = 0.0;  // forward carry into segment g
+#pragma unroll 1
+            for (int t = 0; t < g; ++t) {
+                const double bf = vtab[3 * NV + t * MS + MS - 1];
+                const double2 e = *reinterpret_cast<const double2*>(car + G::ci(t, 2 * kp));
+                ca = fma(bf, ca, e.x);
+                cb = fma(bf, cb, e.y);
+            }
+            double xa = 0.0, xb = 0.0;
+#pragma unroll
+            for (int r = MS - 1; r >= 0; --r) {
+                const double bf = vtab[3 * NV + ag + r], eq = vtab[2 * NV + ag + r];
+                xa = fma(eq, xa, fma(bf, ca, xv[0][r]));
+                xb = fma(eq, xb, fma(bf, cb, xv[1][r]));
+                xv[0][r] = xa;
+                xv[1][r] = xb;
+            }
+            bcast2(SV * G::CP + G::ci(g, 2 * kp), xa, xb);
+        }
+        cluster_sync();
+        {
+            double ca = 0.0, cb = 0.0;  // backward carry into segment g, from the top
+            if (vwork) {
+#pragma unroll 1
+                for (int t = SV - 1; t > g; --t) {
+                    const double bb = vtab[4 * NV + t * MS];
+                    const double2 e = *reinterpret_cast<const double2*>(car + SV * G::CP + G::ci(t, 2 * kp));
+                    ca = fma(bb, ca, e.x);
+                    cb = fma(bb, cb, e.y);
+                }
+#pragma unroll
+                for (int r = 0; r < MS; ++r) {
+                    const double bb = vtab[4 * NV + ag + r];
+                    xv[0][r] = fma(bb, ca, xv[0][r]);
+                    xv[1][r] = fma(bb, cb, xv[1][r]);
+                }
+                // a column on a y Dirichlet face is not solved (solver.cpp:142): its dU1 back
+                if (!vsa || !vsb) {
+                    const double* src = v.D + pb + static_cast<size_t>(slp) * MS * NY + 2 * kp + (vsa ? 1 : 0);
+#pragma unroll
+                    for (int r = 0; r < MS; ++r) {
+                        const double o = __ldg(src + static_cast<size_t>(r) * NY);
+                        if (!vsa) xv[0][r] = o;
+                        else xv[1][r] = o;
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < MS; ++r)
+                *reinterpret_cast<double2*>(tile + G::at(slp * MS + r, 2 * kp)) = make_double2(xv[0][r], xv[1][r]);
+        }
+        __syncthreads();
+    } else if constexpr (REGV) {
         // the table LU's two substitutions as segmented affine scans in
         // registers (TPT independent chains per thread); segment end values go
         // to every CTA of the cluster, each CTA runs the (short) carry chains
