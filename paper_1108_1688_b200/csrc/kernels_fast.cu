@@ -1537,6 +1537,24 @@ __device__ __forceinline__ void bulk_wait(unsigned bar) {
     asm volatile("{\n .reg .pred P;\nWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n"
                  " @!P bra WAIT_%=;\n}" ::"r"(bar) : "memory");
 }
+// remote (cluster) stores that complete on the destination CTA's mbarrier: the
+// consumer waits on its own barrier, no cluster-wide barrier or fence
+__device__ __forceinline__ unsigned map_cluster(unsigned saddr, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_d2(unsigned raddr, double a, double b, unsigned rbar) {
+    asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+                 ::"r"(raddr), "d"(a), "d"(b), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned bar) {  // phase 0, data from peer CTAs
+    asm volatile("{\n .reg .pred P;\nWAITC_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], 0;\n"
+                 " @!P bra WAITC_%=;\n}" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -2192,6 +2210,18 @@ k_plane(BatchView v, int s) {
     const bool live_p = v.dbg || !failed_before(st, s);
     // distributed shared memory of a peer CTA may be written only once the whole
     // cluster is known to be running: arrive here, wait before the first bcast
+    // the v-line carries of a cluster travel as asynchronous remote stores counted
+    // by the receiving CTA's mbarrier (one per direction, used once)
+    __shared__ alignas(8) unsigned long long vbar[2];
+    const unsigned vbar_s = static_cast<unsigned>(__cvta_generic_to_shared(vbar));
+    if constexpr (CS > 1) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(vbar_s) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(vbar_s + 8u) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
     if constexpr (CS > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     auto cluster_sync = [] {
         if constexpr (CS > 1) cg::this_cluster().sync();
@@ -2223,6 +2253,7 @@ k_plane(BatchView v, int s) {
     // adjacent columns of ONE segment instead, so every table value read from
     // shared memory serves two columns and rows move as 128-bit accesses
     constexpr bool VPAIR = REGV && !PAD && TPT == 2 && NT / (NY / 2) == SVL;
+
     const int kp = tid % (NY / 2), slp = tid / (NY / 2);
     double xv[TPT][MS];
     {  // staged even for a failed problem: the loads need not wait for the status word
@@ -2312,13 +2343,25 @@ k_plane(BatchView v, int s) {
         const int ag = g * MS;             // its first row
         const bool vsa = vwork && !(kp == 0 && yminD);
         const bool vsb = vwork && !(kp == NY / 2 - 1 && ymaxD);
-        auto bcast2 = [&](int idx, double va, double vb) {
+        const unsigned car_s = static_cast<unsigned>(__cvta_generic_to_shared(car));
+        auto bcast2 = [&](int d, int idx, double va, double vb) {
             if constexpr (CS > 1) {
 #pragma unroll
                 for (int r = 0; r < CS; ++r)
-                    *reinterpret_cast<double2*>(cg::this_cluster().map_shared_rank(car, r) + idx) = make_double2(va, vb);
+                    st_async_d2(map_cluster(car_s + 8u * idx, r), va, vb, map_cluster(vbar_s + 8u * d, r));
             } else {
                 *reinterpret_cast<double2*>(car + idx) = make_double2(va, vb);
+            }
+        };
+        // every thread of every CTA of the cluster sends one pair per direction
+        auto carry_wait = [&](int d) {
+            if constexpr (CS > 1) {
+                if (vwork) {  // cluster-uniform
+                    if (tid == 0) mbar_expect(vbar_s + 8u * d, CS * NT * 16u);
+                    mbar_wait_cluster(vbar_s + 8u * d);
+                }
+            } else {
+                __syncthreads();
             }
         };
         if (vwork) {
@@ -2341,9 +2384,9 @@ k_plane(BatchView v, int s) {
                 xv[0][r] = la;
                 xv[1][r] = lb;
             }
-            bcast2(G::ci(g, 2 * kp), la, lb);
+            bcast2(0, G::ci(g, 2 * kp), la, lb);
         }
-        cluster_sync();
+        carry_wait(0);
         if (vwork) {
             double ca = 0.0, cb = 0.0;  // forward carry into segment g
 #pragma unroll 1
@@ -2362,9 +2405,9 @@ k_plane(BatchView v, int s) {
                 xv[0][r] = xa;
                 xv[1][r] = xb;
             }
-            bcast2(SV * G::CP + G::ci(g, 2 * kp), xa, xb);
+            bcast2(1, SV * G::CP + G::ci(g, 2 * kp), xa, xb);
         }
-        cluster_sync();
+        carry_wait(1);
         {
             double ca = 0.0, cb = 0.0;  // backward carry into segment g, from the top
             if (vwork) {
@@ -2561,7 +2604,9 @@ k_plane(BatchView v, int s) {
         if constexpr (YLU) {
             // this lane's 16 reciprocal pivots: the warp's block of the table moves
             // as coalesced 128-bit chunks (lane l, chunk q = rows 2q, 2q+1 of its segment)
-            const double2* gq = reinterpret_cast<const double2*>(v.ylu + pb + static_cast<size_t>(jw) * NY);
+            // (HJMSV_DBG bit 64, timing only: every warp reads the table's first block)
+            const double2* gq = reinterpret_cast<const double2*>(
+                v.ylu + ((v.dbg & 64) ? size_t(0) : pb + static_cast<size_t>(jw) * NY));
 #pragma unroll
             for (int q = 0; q < MS / 2; ++q) {
                 const double2 t2 = __ldg(gq + q * 32 + ln);
@@ -3023,7 +3068,7 @@ bool fast_ylu_supported(const BatchView& v) {
         const char* e = std::getenv("HJMSV_YLU");
         return e ? std::atoi(e) : 1;
     }();
-    return on && plane_kernels() == 1 && specialised_shape(v) != 0 && v.fast_step == 0;
+    return on && (plane_kernels() == 1 || plane_kernels() == 3) && specialised_shape(v) != 0 && v.fast_step == 0;
 }
 
 void fast_ylu_build(const BatchView& v, double* ylu, int* flag, cudaStream_t stream) {
@@ -3260,7 +3305,8 @@ void fast_step(const BatchView& v0, int s, cudaStream_t stream, long long* launc
             // 16 warps (512 threads at 128 registers: the y-row coefficients recomputed
             // at each use, U loaded after the solve) — measured faster than 8 warps at
             // 243 registers; HJMSV_PLANE=2: the 8-warp plane; 3: 2-CTA clusters (diagnostics)
-            if (pl == 3) launch_plane<128, 128, 2, 256>(v, s, stream);
+            if (pl == 3 && v.ylu) launch_plane<128, 128, 2, 256, 0, false, true>(v, s, stream);
+            else if (pl == 3) launch_plane<128, 128, 2, 256>(v, s, stream);
             else if (pl == 2) launch_plane<128, 128, 1, 256>(v, s, stream);
             else launch_plane<128, 128, 1, 512>(v, s, stream);
         } else if (pl == 2) launch_plane<256, 256, 4, 256>(v, s, stream);
