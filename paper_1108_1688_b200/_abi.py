@@ -11,7 +11,8 @@ import os
 from ctypes import POINTER, c_double, c_int32, c_int64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libhjmsv_b200.so")
+# HJMSV_LIB: another build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("HJMSV_LIB") or os.path.join(HERE, "lib", "libhjmsv_b200.so")
 
 # hjmsv_status
 OK, INVALID_ARGUMENT, SINGULAR_PIVOT, NONFINITE, DIVERGED, DOMAIN, UNSUPPORTED, CUDA_ERROR, LOGIC = range(9)

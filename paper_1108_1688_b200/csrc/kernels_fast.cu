@@ -1568,6 +1568,11 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     tl_begin(v, s, 0);
     constexpr int M = SEG;
     static_assert(SEG == 16 || (SEG == 32 && TM == 2), "32-row segments keep their arrays in TMEM");
+#ifdef HJMSV_BRFREE_ALL
+    constexpr bool BRFREE = TM == 2;
+#else
+    constexpr bool BRFREE = SEG == 32;  // branch-free march rows
+#endif
     // PAD: any nv, any ny <= NY and any nr <= 512 (the reference's own meshes):
     // the grid's real sizes are runtime values, k lanes past ny and rows past nr
     // run inert (identity rows, no stores); otherwise NV x NY exactly
@@ -1663,7 +1668,8 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     int k = 0;
     bool klive = true, k0 = false, kN = false, solve = false, kface = false, edge = false;
     int eoff = 0;
-    double yk = 0.0, vs6 = 0.0, t6 = 0.0, ths = 0.0, rminv = 0.0, rmaxv = 0.0;
+    double yk = 0.0, vs6 = 0.0, t6 = 0.0, ths = 0.0, rminv = 0.0, rmaxv = 0.0, e3 = 0.0;
+    bool k0o1 = false;
     const double* fyk = fy;
     const double* __restrict__ col = v.U;
     auto tile_k = [&](int t) { return (kt0 + t) * KL + tx; };
@@ -1673,6 +1679,8 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         if (PAD && !klive) k = nyr - 1;  // inert lane: reads a real column, stores nothing
         k0 = k == 0;
         kN = k == nyr - 1;
+        e3 = k0 ? (order2y ? 3.0 : 1.0) : 0.0;
+        k0o1 = k0 && !order2y;
         // is_dirichlet(1,j,k) (solver.cpp:127): the column lies on a v or y Dirichlet face
         solve = klive && !(kN && ymaxD) && !(j == nvr - 1 && dir(v, F_VMAX)) && !(k0 && yminD) &&
                 !(j == 0 && dir(v, F_VMIN));
@@ -1900,11 +1908,25 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                 const unsigned msk = full ? 0xffffffffu : hmask;
                 double kl = __shfl_up_sync(msk, u0, 1, KL);
                 double kr = __shfl_down_sync(msk, u0, 1, KL);
-                if (tx == 0 && !k0) kl = ed;
-                if (tx == KL - 1 && !kN) kr = ed;
-                double yd = kr - kl;
-                if (k0)  // one-sided y row (discretization.cpp:346-352); ed = U(i, j, 2)
-                    yd = order2y ? fma(4.0, kr, -ed) - 3.0 * u0 : 2.0 * (kr - u0);
+                double yd;
+                if constexpr (BRFREE) {
+                    // one-sided y row at k = 0 (discretization.cpp:346-352; ed = U(i, j, 2)) without a
+                    // branch: 4 kr - ed - 3 u0 = (kr - ed) + 3 (kr - u0), and 2 (kr - u0) =
+                    // (kr - u0) + (kr - u0); e3 = 0 on every other column. The unrolled march
+                    // is then one basic block, which the scheduler interleaves across rows
+                    // (config 3 pass A 296 -> 274 us; the register-resident variants spill
+                    // twice as much that way and keep the branch)
+                    if (tx == 0) kl = ed;
+                    if (k0o1) kl = u0;
+                    if (tx == KL - 1 && !kN) kr = ed;
+                    yd = fma(e3, kr - u0, kr - kl);
+                } else {
+                    if (tx == 0 && !k0) kl = ed;
+                    if (tx == KL - 1 && !kN) kr = ed;
+                    yd = kr - kl;
+                    if (k0)  // one-sided y row (discretization.cpp:346-352); ed = U(i, j, 2)
+                        yd = order2y ? fma(4.0, kr, -ed) - 3.0 * u0 : 2.0 * (kr - u0);
+                }
                 acc = fma(fma(a_i, vs6, t6), yd, acc);
                 return acc * dtm;  // y-face Dirichlet columns are fixed up after the march
             };
