@@ -2830,6 +2830,63 @@ k_plane(BatchView v, int s) {
                 if (sy < LY - 1) right = rg;
             }
         }
+        // CTAIL: the update runs in the coalesced order (measured faster on 64-, 128-
+        // and 256-wide planes, slower on the 32-wide planes of config 4)
+        constexpr bool CTAIL = YLU && NY >= 64;
+        if constexpr (CTAIL) {
+            // dU3: the right carry times the product of -c' down to each row
+            double b = right;  // 0 on lines that are not solved (they keep dU2)
+#pragma unroll
+            for (int r = MS - 1; r >= 0; --r) {
+                b *= -cs[r];
+                x[r] += b;
+            }
+            if (wmd) {
+#pragma unroll
+                for (int r = 0; r < MS; ++r) md = fmax(md, fabs(x[r]));
+            }
+            // U += dU3 in the coalesced order: only dU3 crosses the warp's tile rows
+            // (each lane overwrites the segment it read), U stays in registers as
+            // 128-bit chunks from load to store
+#pragma unroll
+            for (int q = 0; q < MS / 2; ++q)
+                *reinterpret_cast<double2*>(tile + G::at(jl, a + 2 * q)) = make_double2(x[2 * q], x[2 * q + 1]);
+            if constexpr (!early_u) load_us();
+            __syncwarp();
+            unsigned hm = 0u;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int e = q * 64 + 2 * ln;
+                const int jr = jw + e / NY, k = e % NY, jg = j0 + jr;
+                const double2 d2 = *reinterpret_cast<const double2*>(tile + G::at(jr, k));
+                double2 u2 = make_double2(us[q].x + d2.x, us[q].y + d2.y);
+                // Dirichlet nodes take their closed-form values at t_next (solver.cpp:169-174)
+                if (planeD || (jg == 0 && vminD) || (jg == nvr - 1 && vmaxD)) {
+                    u2.x = fval(v, p, dface(v, i, jg, k), i, k);
+                    u2.y = fval(v, p, dface(v, i, jg, k + 1), i, k + 1);
+                } else {
+                    if (k == 0 && yminD) u2.x = vtab[6 * NV + 1];
+                    if (k + 1 == NY - 1 && ymaxD) u2.y = vtab[6 * NV];
+                }
+                us[q] = u2;
+                hm = max(hm, max(static_cast<unsigned>(__double2hiint(u2.x)) & 0x7fffffffu,
+                                 static_cast<unsigned>(__double2hiint(u2.y)) & 0x7fffffffu));
+            }
+            // guard_finite (solver.cpp:69-77): one integer max decides for the lane's 16 values
+            if (!(v.dbg & 32) && hm >= static_cast<unsigned>(__double2hiint(bound))) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int e = q * 64 + 2 * ln;
+                    const unsigned long long flat =
+                        (static_cast<unsigned long long>(i) * nvr + j0 + jw + e / NY) * nyr + e % NY;
+                    if (!(fabs(us[q].x) <= bound)) guard_fail(v, p, s, flat, us[q].x);
+                    if (!(fabs(us[q].y) <= bound)) guard_fail(v, p, s, flat + 1, us[q].y);
+                }
+            }
+            double2* gw = reinterpret_cast<double2*>(v.U + pb + static_cast<size_t>(jw) * NY);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) gw[q * 32 + ln] = us[q];
+        } else
         if (live) {
             if constexpr (stage_u) {
                 if constexpr (!early_u) load_us();
@@ -2857,9 +2914,9 @@ k_plane(BatchView v, int s) {
                     b *= -cs[r];
                     dq = x[r] + b;
                 } else {
-                if constexpr (G::MINB == 1) b = cs[r];  // the twisted solve left beta itself
-                else if (r < MS - 1) b = -cs[r] * b;
-                dq = fma(b, right, fma(al[r], left, x[r]));
+                    if constexpr (G::MINB == 1) b = cs[r];  // the twisted solve left beta itself
+                    else if (r < MS - 1) b = -cs[r] * b;
+                    dq = fma(b, right, fma(al[r], left, x[r]));
                 }
                 un[r] += dq;
                 x[r] = dq;
