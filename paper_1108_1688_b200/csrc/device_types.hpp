@@ -85,6 +85,12 @@ struct BatchView {
     // steps): 1 / pivot of the reference's Thomas elimination (solver.cpp:42-50)
     // per node, [P][N] in pass B's warp-block order (fast_ylu_build), or null
     const double* ylu;
+    // pass B: every CTA asks L2 for the dU1 rows of the plane pf_ahead planes on (the
+    // plane its SM is likely to get next) while its own y phase runs; 0: off
+    int pf_ahead;
+    // pass A: the same for the U column of the CTA pf_ahead_a CTAs on, asked for
+    // once this CTA's march has ended; 0: off
+    int pf_ahead_a;
 };
 constexpr int kTlSlots = 5;  // 0 pass A / explicit, 1 r-lines, 2 pass B / v-lines, 3 y-lines, 4 faces
 

@@ -28,7 +28,9 @@
 // reduced pivots stand in for the global ones in the singular-pivot check.
 // Parity with the reference is 1e-10 normwise (tests/test_gpu_parity.py).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <set>
 #include <tuple>
@@ -2026,6 +2028,22 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         if (jdeg) march(std::true_type{});
         else march(std::false_type{});
         if (!ok) record_pivot(st, s, 0, j * nyr + k, a + bad_r);
+        // the next wave's U column -> L2: one 128-byte line per row of this thread's
+        // segment, asked for now that this CTA's own window traffic has ended
+        // (compiled into the tensor-memory variants only: the register-resident ones
+        // of the small planes lose 2 % to the extra code and keep their grids in L2)
+        if constexpr (!PAD && TPC == 1 && KL == 16 && TM == 2) {
+            if (v.pf_ahead_a && tx == 0) {
+                const unsigned nb = blockIdx.x + static_cast<unsigned>(v.pf_ahead_a);
+                if (nb < gridDim.x) {
+                    const unsigned j2 = nb / TK, kt2 = nb - j2 * TK;
+                    const double* c2 = v.U + off + static_cast<size_t>(j2) * NY + kt2 * KL + static_cast<size_t>(a) * SR;
+#pragma unroll
+                    for (int r = 0; r < M; ++r)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(c2 + static_cast<size_t>(r) * SR));
+                }
+            }
+        }
         // reduced-system rows as [column][field][segment] (field stride S+1, column
         // stride 8S+9: conflict-free for the writers, lanes = k, and for the
         // scans, lanes = segments)
@@ -2277,9 +2295,13 @@ k_plane(BatchView v, int s) {
     constexpr bool VPAIR = REGV && !PAD && TPT == 2 && NT / (NY / 2) == SVL;
 
     const int kp = tid % (NY / 2), slp = tid / (NY / 2);
+    constexpr bool LATE_PF = VPAIR;
     double xv[TPT][MS];
     {  // staged even for a failed problem: the loads need not wait for the status word
-        if (!PAD && tid == 0) {  // U rows -> L2 early, so the update's loads hit L2
+        // U (and pivot) rows -> L2 ahead of the update, so its loads hit L2; the
+        // column-pair variant asks for them once its dU1 loads have landed (LATE_PF),
+        // so the two streams do not share DRAM bandwidth and the v phase keeps DRAM busy
+        if (!PAD && tid == 0 && !LATE_PF) {
             constexpr unsigned bytes = RV * NY * sizeof(double);
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.U + pb), "r"(bytes) : "memory");
             if constexpr (YLU)
@@ -2408,6 +2430,12 @@ k_plane(BatchView v, int s) {
             }
             bcast2(0, G::ci(g, 2 * kp), la, lb);
         }
+        if (LATE_PF && tid == 0) {
+            constexpr unsigned bytes = RV * NY * sizeof(double);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.U + pb), "r"(bytes) : "memory");
+            if constexpr (YLU)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.ylu + pb), "r"(bytes) : "memory");
+        }
         carry_wait(0);
         if (vwork) {
             double ca = 0.0, cb = 0.0;  // forward carry into segment g
@@ -2460,6 +2488,15 @@ k_plane(BatchView v, int s) {
 #pragma unroll
             for (int r = 0; r < MS; ++r)
                 *reinterpret_cast<double2*>(tile + G::at(slp * MS + r, 2 * kp)) = make_double2(xv[0][r], xv[1][r]);
+        }
+        // the next wave's dU1 rows -> L2 while this CTA's y phase leaves DRAM idle
+        if (v.pf_ahead && tid == 0) {
+            const long long w2 = static_cast<long long>(w) + v.pf_ahead;
+            if (w2 < static_cast<long long>(nr) * v.P) {
+                constexpr unsigned bytes = RV * NY * sizeof(double);
+                const double* nx = v.D + (static_cast<size_t>(w2) * NV + j0) * NY;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx), "r"(bytes) : "memory");
+            }
         }
         __syncthreads();
     } else if constexpr (REGV) {
@@ -3022,6 +3059,41 @@ int pdl_enabled() {
     return on;
 }
 
+// CTAs of a kernel resident on the current device at once (cached per device,
+// kernel and launch shape): the distance of the next-wave L2 prefetches
+int resident_ctas(const void* fn, int threads, size_t smem) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int, size_t>, int> memo;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(dev, fn, threads, smem);
+    const auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    // from the kernel's own resources (the occupancy API answers for the current
+    // shared-memory carveout, not the one the launch will get)
+    int per_sm = 0, sms = 0, regs_sm = 0, thr_sm = 0, smem_sm = 0, blk_sm = 0;
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&blk_sm, cudaDevAttrMaxBlocksPerMultiprocessor, dev) == cudaSuccess) {
+        const int warps = (threads + 31) / 32;
+        const int regs_cta = ((fa.numRegs * 32 + 255) / 256 * 256) * warps;  // warp granularity 256
+        const size_t smem_cta = smem + fa.sharedSizeBytes + 1024;            // + the per-CTA reserve
+        per_sm = std::min({blk_sm, thr_sm / threads, regs_cta ? regs_sm / regs_cta : blk_sm,
+                           static_cast<int>(static_cast<size_t>(smem_sm) / smem_cta)});
+    } else {
+        cudaGetLastError();
+        per_sm = sms = 0;
+    }
+    if (std::getenv("HJMSV_TIMING"))
+        std::fprintf(stderr, "[hjmsv] resident CTAs: %d per SM x %d SMs (threads %d, smem %zu)\n", per_sm, sms, threads, smem);
+    return memo[key] = per_sm * sms;
+}
+
 template <class K>
 void launch_pdl(K kernel, dim3 g, dim3 b, size_t sm, cudaStream_t stream, const BatchView& v, int s) {
     cudaLaunchConfig_t cfg = {};
@@ -3034,7 +3106,15 @@ void launch_pdl(K kernel, dim3 g, dim3 b, size_t sm, cudaStream_t stream, const 
     at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kernel, v, s);
+    // next-wave prefetch distance: the CTAs resident at once (HJMSV_PF_AHEAD_A: 0 off, n fixed)
+    BatchView w = v;
+    static const int pfa_env = [] {
+        const char* e = std::getenv("HJMSV_PF_AHEAD_A");
+        return e ? std::atoi(e) : -1;
+    }();
+    w.pf_ahead_a = pfa_env >= 0 ? pfa_env : resident_ctas(reinterpret_cast<const void*>(kernel), b.x * b.y * b.z, sm);
+    if (static_cast<long long>(g.x) <= w.pf_ahead_a) w.pf_ahead_a = 0;  // one wave: nothing to prefetch
+    cudaLaunchKernelEx(&cfg, kernel, w, s);
 }
 
 // The pivots of every y-line of a constant-model batch in the reference's Thomas
@@ -3111,7 +3191,41 @@ void launch_plane(const BatchView& v, int s, cudaStream_t stream) {
     at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    cudaLaunchKernelEx(&cfg, k_plane<NV, NY, CS, NT, MB, PAD, YLU>, v, s);
+    // next-wave prefetch distance: the clusters (planes) resident at once
+    // (HJMSV_PF_AHEAD: 0 off, n fixed); measured on config 3: 33 resident, 30 / 33
+    // planes ahead 291 -> 271 us, 66 ahead 295 us
+    BatchView w = v;
+    static const int pf_env = [] {
+        const char* e = std::getenv("HJMSV_PF_AHEAD");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (pf_env >= 0) {
+        w.pf_ahead = pf_env;
+    } else {
+        static std::mutex mu;
+        static std::map<int, int> memo;  // per device, for this instantiation
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(mu);
+        const auto it = memo.find(dev);
+        if (it != memo.end()) {
+            w.pf_ahead = it->second;
+        } else {
+            int n = 0;
+            if (CS > 1) {
+                if (cudaOccupancyMaxActiveClusters(&n, k_plane<NV, NY, CS, NT, MB, PAD, YLU>, &cfg) != cudaSuccess) {
+                    cudaGetLastError();
+                    n = 0;
+                }
+            } else {
+                n = resident_ctas(reinterpret_cast<const void*>(k_plane<NV, NY, CS, NT, MB, PAD, YLU>), NT,
+                                  G::SMEM + pb_pad);
+            }
+            w.pf_ahead = memo[dev] = n;
+        }
+    }
+    if (static_cast<long long>(v.nr) * v.P <= w.pf_ahead) w.pf_ahead = 0;  // one wave
+    cudaLaunchKernelEx(&cfg, k_plane<NV, NY, CS, NT, MB, PAD, YLU>, w, s);
 }
 
 int plane_kernels() {
