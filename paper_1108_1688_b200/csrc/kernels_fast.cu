@@ -1553,8 +1553,12 @@ __device__ __forceinline__ void st_async_d2(unsigned raddr, double a, double b, 
 __device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait_cluster(unsigned bar) {  // phase 0, data from peer CTAs
-    asm volatile("{\n .reg .pred P;\nWAITC_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], 0;\n"
+// phase 0 of a barrier that counts st.async bytes from peer CTAs: the completion
+// of the transaction makes the stored data visible to the waiting thread, as
+// for bulk copies (an acquire at cluster scope would invalidate all of L1:
+// CCTL.IVALL, 6 % of pass B's stall samples when it was tried)
+__device__ __forceinline__ void mbar_wait_cluster(unsigned bar) {
+    asm volatile("{\n .reg .pred P;\nWAITC_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n"
                  " @!P bra WAITC_%=;\n}" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -2489,15 +2493,6 @@ k_plane(BatchView v, int s) {
             for (int r = 0; r < MS; ++r)
                 *reinterpret_cast<double2*>(tile + G::at(slp * MS + r, 2 * kp)) = make_double2(xv[0][r], xv[1][r]);
         }
-        // the next wave's dU1 rows -> L2 while this CTA's y phase leaves DRAM idle
-        if (v.pf_ahead && tid == 0) {
-            const long long w2 = static_cast<long long>(w) + v.pf_ahead;
-            if (w2 < static_cast<long long>(nr) * v.P) {
-                constexpr unsigned bytes = RV * NY * sizeof(double);
-                const double* nx = v.D + (static_cast<size_t>(w2) * NV + j0) * NY;
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx), "r"(bytes) : "memory");
-            }
-        }
         __syncthreads();
     } else if constexpr (REGV) {
         // the table LU's two substitutions as segmented affine scans in
@@ -2607,6 +2602,15 @@ k_plane(BatchView v, int s) {
             }
         }
         __syncthreads();
+    }
+    // the next wave's dU1 rows -> L2 while this CTA's y phase leaves DRAM idle
+    if (!PAD && v.pf_ahead && tid == 0) {
+        const long long w2 = static_cast<long long>(w) + v.pf_ahead;
+        if (w2 < static_cast<long long>(nr) * v.P) {
+            constexpr unsigned bytes = RV * NY * sizeof(double);
+            const double* nx = v.D + (static_cast<size_t>(w2) * NV + j0) * NY;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx), "r"(bytes) : "memory");
+        }
     }
     if (!live_p) return;  // no cluster barrier follows
 

@@ -412,11 +412,14 @@ print("WORST", worst)
 
 @pytest.mark.parametrize("env", [{"HJMSV_PLANE": "0"}, {"HJMSV_PLANE": "0", "HJMSV_PA": "0"},
                                  {"HJMSV_PLANE": "3"}, {"HJMSV_PLANE": "2"}, {"HJMSV_DBG": "2"},
-                                 {"HJMSV_PA_TM": "0", "HJMSV_PA_SEG": "16"}])
+                                 {"HJMSV_PA_TM": "0", "HJMSV_PA_SEG": "16"},
+                                 {"HJMSV_YLU": "0"}, {"HJMSV_PF_AHEAD": "0", "HJMSV_PF_AHEAD_A": "0"},
+                                 {"HJMSV_PF_AHEAD": "3", "HJMSV_PF_AHEAD_A": "5"}])
 def test_diagnostic_schedules(gpu, env):
     """The schedules behind the diagnostic switches (split v + y kernels with the
     lane-scan k_y3, the four-kernel schedule, the 2-CTA cluster plane, pass A's
-    two-ended recurrence at 16+ segments) stay at parity. The switches are read
+    two-ended recurrence at 16+ segments, pass B's partition-method y-lines instead
+    of the pivot table, the next-wave prefetches off or at odd distances) stay at parity. The switches are read
     once per process, so each runs in its own interpreter."""
     import os
     import subprocess
