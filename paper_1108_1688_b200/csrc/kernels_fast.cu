@@ -1573,6 +1573,11 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     tl_begin(v, s, 0);
     constexpr int M = SEG;
+    // FOLD (the 32-row variant: 512-row lines): the (step, j) part of a row's
+    // coefficients folded into the CTA's r-table. Config 3 pass A 265 -> 261 us;
+    // on shorter lines the per-CTA table pass costs more than it saves (config 1
+    // +7 %, configs 2 / 4 +6-8 %)
+    constexpr bool FOLD = SEG == 32;
     static_assert(SEG == 16 || (SEG == 32 && TM == 2), "32-row segments keep their arrays in TMEM");
 #ifdef HJMSV_BRFREE_ALL
     constexpr bool BRFREE = TM == 2;
@@ -1667,6 +1672,9 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     // one-sided 2 g5 (u_{j+1} - u_j) term, and the cross term vanishes
     const bool jdeg = jlo && !jdir;
     if (jdeg) v01.y = v23.x;
+    // FOLD: the stencil's coefficients carry dt, the line coefficients theta dt / dt
+    const double g2c = FOLD ? v01.y * dtm : v01.y, g5c = FOLD ? v23.x * dtm : v23.x;
+    const double thc = FOLD ? th / dtm : th;
     const bool order2y = v.y_order != 1, order2r = v.r_order != 1;
     const double* fbp = v.fb + static_cast<size_t>(p) * v.fb_stride;
 
@@ -1693,8 +1701,8 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         const double2* Y2 = reinterpret_cast<const double2*>(F.Y + kFY * k);
         const double2 y01 = __ldg(Y2), y23 = __ldg(Y2 + 1);  // (S6, T6), (Y, pad)
         yk = y23.x;
-        vs6 = vj * y01.x;
-        t6 = y01.y;
+        vs6 = FOLD ? y01.x : vj * y01.x;
+        t6 = FOLD ? y01.y * dtm : y01.y;
         fyk = fy + (kN ? 0 : nr);
         kface = (kN && ymaxD) || (k0 && yminD);
         // r-face values this thread needs (first / last segment)
@@ -1706,7 +1714,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         edge = klive && (tx == 0 || (tx == KL - 1 && !kN));
         eoff = tx == 0 ? (k0 ? 2 : -1) : 1;
         // interior rows (0 < i < nr-1); a column that is not solved runs identity rows
-        ths = solve ? th : 0.0;
+        ths = solve ? thc : 0.0;
     };
     tile_setup(0);
     double x[M], cs[M], al[M];
@@ -1801,6 +1809,26 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         }
     };
     bulk_wait(tbar_s);  // rt, fy have landed
+    // FOLD: everything of a row's coefficients that depends on (step, j) only is
+    // folded into this CTA's copy of the r-table, scaled by dt:
+    //   (G1 v_j dt, (c4 G4C + G4V v_j + G4P) dt | G4Q dt, G3 G3V_j dt | REACT dt, A v_j dt)
+    // so a march row reads three 128-bit pairs and builds g4 with one FMA
+    if constexpr (FOLD) {
+        if (!jdir) {
+            for (int i = tid; i < nr; i += nt) {
+                double* R = rt + kFR * i;
+                const double g1 = R[FR_G1], g4c = R[FR_G4C], g4p = R[FR_G4P], g4q = R[FR_G4Q], g4v = R[FR_G4V],
+                             g3 = R[FR_G3], re = R[FR_REACT], aa = R[FR_A];
+                R[0] = g1 * vj * dtm;
+                R[1] = fma(c4, g4c, fma(g4v, vj, g4p)) * dtm;
+                R[2] = g4q * dtm;
+                R[3] = g3 * v23.y * dtm;
+                R[4] = re * dtm;
+                R[5] = aa * vj * dtm;
+            }
+        }
+        __syncthreads();
+    }
     if (fail) {  // the problem failed in an earlier step (block-uniform)
         cp_async_wait<0>();
         tm_free();
@@ -1842,15 +1870,15 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
         if (!solve || (i == nr - 1 && rmaxD) || (i == 0 && rminD)) return;
         if (i == 0) {
             if (!order2r) {
-                d = fma(2.0 * th, g4h, 1.0);
-                u = -2.0 * th * g4h;
+                d = fma(2.0 * thc, g4h, 1.0);
+                u = -2.0 * thc * g4h;
             } else {
-                d = fma(3.0 * th, g4h, 1.0);
-                u = -4.0 * th * g4h;
-                s2 = th * g4h;
+                d = fma(3.0 * thc, g4h, 1.0);
+                u = -4.0 * thc * g4h;
+                s2 = thc * g4h;
             }
         } else {
-            const double w2 = th * g1s, w1 = th * g4h;
+            const double w2 = thc * g1s, w1 = thc * g4h;
             l = w1 - w2;
             d = fma(2.0, w2, 1.0);
             u = -(w2 + w1);
@@ -1864,12 +1892,19 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
     };
     auto rtab = [&](int i, double2& r01, double2& r23, double2& r45, double2& r67) {
         const double2* R2 = reinterpret_cast<const double2*>(rt + kFR * i);
-        r01 = R2[0]; r23 = R2[1]; r45 = R2[2]; r67 = R2[3];
-        // r01 = (G1, G4C), r23 = (G4P, G4Q), r45 = (G4V, G3), r67 = (REACT, A)
+        r01 = R2[0]; r23 = R2[1]; r45 = R2[2];
+        if constexpr (!FOLD) r67 = R2[3];
+        // r01 = (G1, G4C), r23 = (G4P, G4Q), r45 = (G4V, G3), r67 = (REACT, A); FOLD:
+        // r01 = (G1 v dt, g4 part dt), r23 = (G4Q dt, G3 G3V dt), r45 = (REACT dt, A v dt)
     };
     auto g4 = [&](const double2& r01, const double2& r23, const double2& r45) {
-        return fma(c4, r01.y, fma(r23.y, yk, fma(r45.x, vj, r23.x)));
+        if constexpr (FOLD) return fma(r23.x, yk, r01.y);
+        else return fma(c4, r01.y, fma(r23.y, yk, fma(r45.x, vj, r23.x)));
     };
+    auto g1v = [&](const double2& r01) { return FOLD ? r01.x : r01.x * vj; };
+    auto g3c = [&](const double2& r23, const double2& r45) { return FOLD ? r23.y : r45.y * v23.y; };
+    auto rea = [&](const double2& r45, const double2& r67) { return FOLD ? r45.x : r67.x; };
+    auto aiv = [&](const double2& r45, const double2& r67) { return FOLD ? r45.y : r67.y; };
 
     const int FS = S + 1, CST = 8 * S + 9;
 #pragma unroll 1
@@ -1934,20 +1969,20 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                         yd = order2y ? fma(4.0, kr, -ed) - 3.0 * u0 : 2.0 * (kr - u0);
                 }
                 acc = fma(fma(a_i, vs6, t6), yd, acc);
-                return acc * dtm;  // y-face Dirichlet columns are fixed up after the march
+                return FOLD ? acc : acc * dtm;  // y-face Dirichlet columns are fixed up after the march
             };
             // dU0 at an interior row i from a window (mm, cc, pp)
-            auto stencil = [&](bool full, const double2& r01, const double2& r45, const double2& r67,
+            auto stencil = [&](bool full, const double2& r01, const double2& r23, const double2& r45, const double2& r67,
                                double g4h, double mqx, double mq1, double cq0, double cq1,
                                double cq2, double pq0, double pq1, double pq2, double ed) {
                 const double u0 = cq1;
-                double acc = -r67.x * u0;
-                acc = fma(r01.x * vj, (pq1 + mq1) - 2.0 * u0, acc);
+                double acc = -rea(r45, r67) * u0;
+                acc = fma(g1v(r01), (pq1 + mq1) - 2.0 * u0, acc);
                 acc = fma(g4h, pq1 - mq1, acc);
-                acc = fma(v01.y, (cq2 + cq0) - 2.0 * u0, acc);
-                acc = fma(v23.x, cq2 - cq0, acc);
-                acc = fma(r45.y * v23.y, (pq2 - pq0) - mqx, acc);
-                return yterm(full, u0, acc, r67.y, ed);
+                acc = fma(g2c, (cq2 + cq0) - 2.0 * u0, acc);
+                acc = fma(g5c, cq2 - cq0, acc);
+                acc = fma(g3c(r23, r45), (pq2 - pq0) - mqx, acc);
+                return yterm(full, u0, acc, aiv(r45, r67), ed);
             };
             auto row = [&](int r, double& l, double& d, double& u) {
                 const int i = a + r;
@@ -1960,11 +1995,11 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                         cp_async_wait<kRing - 1>();  // row 2 (ring slot 0)
                         const double n0 = *slot(0, 0), n1 = *slot(0, 1), n2 = *slot(0, 2);
                         const double u0 = c1;
-                        double acc = -r67.x * u0;
+                        double acc = -rea(r45, r67) * u0;
                         acc = fma(g4h, order2r ? fma(4.0, p1, -n1) - 3.0 * u0 : 2.0 * (p1 - u0), acc);
-                        acc = fma(v01.y, (c2 + c0) - 2.0 * u0, acc);
-                        acc = fma(v23.x, c2 - c0, acc);
-                        double x0 = yterm(false, u0, acc, r67.y, ce);
+                        acc = fma(g2c, (c2 + c0) - 2.0 * u0, acc);
+                        acc = fma(g5c, c2 - c0, acc);
+                        double x0 = yterm(false, u0, acc, aiv(r45, r67), ce);
                         // r_min Dirichlet ranks below r_max / y_max / v_max (discretization.cpp:153-192)
                         if (rminD && !(kN && ymaxD)) x0 = rminv - u0;
                         x[0] = x0;
@@ -1972,12 +2007,12 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                         double2 q01, q23, q45, q67;
                         rtab(1, q01, q23, q45, q67);
                         const double g4h1 = g4(q01, q23, q45);
-                        const double x1 = stencil(false, q01, q45, q67, g4h1, c2 - c0, c1, p0, p1, p2, n0, n1, n2, pe);
+                        const double x1 = stencil(false, q01, q23, q45, q67, g4h1, c2 - c0, c1, p0, p1, p2, n0, n1, n2, pe);
                         double d0, u0c, s20, l1, d1, u1, t1, l0;
-                        coeffs(0, r01.x * vj, g4h, l0, d0, u0c, s20);
+                        coeffs(0, g1v(r01), g4h, l0, d0, u0c, s20);
                         double f0d = d0, f0u = u0c;
                         if (s20 != 0.0) {
-                            coeffs(1, q01.x * vj, g4h1, l1, d1, u1, t1);
+                            coeffs(1, g1v(q01), g4h1, l1, d1, u1, t1);
                             if (fabs(u1) > 1e-300) {
                                 const double f = s20 / u1;
                                 f0d = fma(-f, l1, d0);
@@ -1987,7 +2022,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                                 cp_async_wait<kRing - 2>();
                                 double2 w01, w23, w45, w67;
                                 rtab(2, w01, w23, w45, w67);
-                                const double x2 = stencil(false, w01, w45, w67, g4(w01, w23, w45), p2 - p0, p1, n0,
+                                const double x2 = stencil(false, w01, w23, w45, w67, g4(w01, w23, w45), p2 - p0, p1, n0,
                                                           n1, n2, *slot(1, 0), *slot(1, 1), *slot(1, 2),
                                                           edge ? *slot(0, 3) : 0.0);
                                 x[0] = fma(-s20, x2, x[0]);
@@ -1996,10 +2031,10 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                         l = 0.0; d = f0d; u = f0u;
                         return;
                     }
-                    x[0] = stencil(false, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
+                    x[0] = stencil(false, r01, r23, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
                 } else {
                     shift(r);
-                    const double xv = stencil(true, r01, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
+                    const double xv = stencil(true, r01, r23, r45, r67, g4h, mx, m1, c0, c1, c2, p0, p1, p2, ce);
                     // face plane i = nr-1: r_max is always Dirichlet and ranks first
                     // (PAD: rows past nr-1 are inert identity rows)
                     if constexpr (PAD) x[r] = xv;
@@ -2013,7 +2048,7 @@ __global__ void __launch_bounds__(512) k_pa(BatchView v, int s) {
                 if (PAD ? (i >= nr - 1 && (i > nr - 1 || rmaxD)) : (r == M - 1 && i == nr - 1 && rmaxD)) {
                     l = 0.0; d = 1.0; u = 0.0;
                 } else {
-                    interior(r01.x * vj, g4h, l, d, u);
+                    interior(g1v(r01), g4h, l, d, u);
                 }
             };
             if constexpr (TM == 2) ok = seg_solve_tm2<M>(x, taddr, yF, aF, bF, yL, aL, bL, bad_r, row);
