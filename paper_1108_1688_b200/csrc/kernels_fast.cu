@@ -2471,7 +2471,6 @@ k_plane(BatchView v, int s) {
         }
         if (LATE_PF && tid == 0) {
             constexpr unsigned bytes = RV * NY * sizeof(double);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.U + pb), "r"(bytes) : "memory");
             if constexpr (YLU)
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.ylu + pb), "r"(bytes) : "memory");
         }
@@ -2638,15 +2637,23 @@ k_plane(BatchView v, int s) {
         }
         __syncthreads();
     }
+    // (the U rows only now: the v phase's DRAM time went to the pivot rows)
+    if (LATE_PF && tid == 0) {
+        constexpr unsigned bytes = RV * NY * sizeof(double);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v.U + pb), "r"(bytes) : "memory");
+    }
     // the next wave's dU1 rows -> L2 while this CTA's y phase leaves DRAM idle
-    if (!PAD && v.pf_ahead && tid == 0) {
+    auto next_wave = [&] {
         const long long w2 = static_cast<long long>(w) + v.pf_ahead;
         if (w2 < static_cast<long long>(nr) * v.P) {
             constexpr unsigned bytes = RV * NY * sizeof(double);
             const double* nx = v.D + (static_cast<size_t>(w2) * NV + j0) * NY;
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx), "r"(bytes) : "memory");
         }
-    }
+    };
+    // (measured on config 3: after the second carry broadcast or after the first
+    // y round instead: 268 against 260.5 us)
+    if (!PAD && v.pf_ahead && tid == 0) next_wave();
     if (!live_p) return;  // no cluster barrier follows
 
     // ---- y-lines (rows j) + update, in rounds of NT segment tasks
