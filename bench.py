@@ -422,7 +422,9 @@ def main():
                     "kernels": [{"name": k["name"], "avg_us": 1e3 * k["avg_ms"],
                                  "share_of_step": k["avg_ms"] * (1 if k["name"] == "fx_faces" else steps_per_march)
                                  / prof_ms,
-                                 "alg_GBps": k["alg_bytes"] / (k["avg_ms"] / 1e3) / 1e9 if k["avg_ms"] else None}
+                                 "alg_GBps": k["alg_bytes"] / (k["avg_ms"] / 1e3) / 1e9 if k["avg_ms"] else None,
+                                 "frac": k["alg_bytes"] / (k["avg_ms"] / 1e3) / 1e9 / peak if k["avg_ms"] else None,
+                                 "traffic": ncu_traffic(args.config, k["name"])}
                                 for k in prof]}
 
     # end to end through the C-ABI with host buffers
