@@ -3140,6 +3140,19 @@ int resident_ctas(const void* fn, int threads, size_t smem) {
     return memo[key] = per_sm * sms;
 }
 
+// the arrays a march touches every step (U, dU, the pivot table) fit the L2 of the
+// current device: next-wave prefetches have nothing to hide (config 1: 100 MB of 126 MB)
+bool fits_l2(const BatchView& v) {
+    int dev = 0, l2 = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    const double bytes = static_cast<double>(v.P) * static_cast<double>(v.N) * sizeof(double) * (v.ylu ? 3.0 : 2.0);
+    return bytes <= static_cast<double>(l2);
+}
+
 template <class K>
 void launch_pdl(K kernel, dim3 g, dim3 b, size_t sm, cudaStream_t stream, const BatchView& v, int s) {
     cudaLaunchConfig_t cfg = {};
@@ -3160,6 +3173,7 @@ void launch_pdl(K kernel, dim3 g, dim3 b, size_t sm, cudaStream_t stream, const 
     }();
     w.pf_ahead_a = pfa_env >= 0 ? pfa_env : resident_ctas(reinterpret_cast<const void*>(kernel), b.x * b.y * b.z, sm);
     if (static_cast<long long>(g.x) <= w.pf_ahead_a) w.pf_ahead_a = 0;  // one wave: nothing to prefetch
+    if (pfa_env < 0 && fits_l2(v)) w.pf_ahead_a = 0;  // the march's arrays stay in L2 anyway
     cudaLaunchKernelEx(&cfg, kernel, w, s);
 }
 
