@@ -2810,8 +2810,7 @@ k_plane(BatchView v, int s) {
             }
             right = __shfl_down_sync(FULL, bb, 1, LY);  // x_{a+16}; its multipliers are applied below
             if (sy == LY - 1 || !solve) right = 0.0;
-        } else
-        if (solve && !(v.dbg & 4)) {
+        } else if (solve && !(v.dbg & 4)) {
             const double h1 = a_i * vtab[5 * NV + j];
             // th g6 / (2 dxy) per row: a table (8-warp CTAs) or recomputed at each use
             // (16-warp CTAs, whose 128 registers hold the solve's arrays)
@@ -2880,8 +2879,8 @@ k_plane(BatchView v, int s) {
         // the line's reduced system: its LY segments are LY consecutive lanes of
         // one warp, solved by a lane scan (shuffles only)
         if constexpr (YLU) {
-        } else
-        if constexpr (LY > 1 && LY < 8) {
+            // (the table-driven solve above resolved the carries by its own lane scans)
+        } else if constexpr (LY > 1 && LY < 8) {
             // short systems: one lane per line through shared memory (measured
             // faster than the scan for 2 and 4 segments), rows as
             // [segment][field][line] (padded, bank-conflict free)
@@ -2969,8 +2968,7 @@ k_plane(BatchView v, int s) {
             double2* gw = reinterpret_cast<double2*>(v.U + pb + static_cast<size_t>(jw) * NY);
 #pragma unroll
             for (int q = 0; q < 8; ++q) gw[q * 32 + ln] = us[q];
-        } else
-        if (live) {
+        } else if (live) {
             if constexpr (stage_u) {
                 if constexpr (!early_u) load_us();
                 __syncwarp();  // every lane has read its x from the warp's tile rows
