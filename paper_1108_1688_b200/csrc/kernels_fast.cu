@@ -622,17 +622,18 @@ __device__ __forceinline__ int reduced_scan(double yF, double aF, double bF, dou
         const double q12 = __shfl_up_sync(FULL, n12, off, L);
         const double q21 = __shfl_up_sync(FULL, n21, off, L);
         const double q22 = __shfl_up_sync(FULL, n22, off, L);
-        if (t >= off) {
+        {  // selects instead of a branch: the levels schedule as one block
             const double d11 = fma(n11, q11, n12 * q21);
             const double d12 = fma(n11, q12, n12 * q22);
             const double d21 = fma(n21, q11, n22 * q21);
             const double d22 = fma(n21, q12, n22 * q22);
-            n11 = d11; n12 = d12; n21 = d21; n22 = d22;
-            const int ex = (__double2hiint(n22) >> 20) & 0x7ff;
-            if (ex != 0 && ex != 0x7ff) {
-                const double sc = __hiloint2double((2046 - ex) << 20, 0);  // 2^(1023 - ex)
-                n11 *= sc; n12 *= sc; n21 *= sc; n22 *= sc;
-            }
+            const int ex = (__double2hiint(d22) >> 20) & 0x7ff;
+            const double sc = (ex != 0 && ex != 0x7ff) ? __hiloint2double((2046 - ex) << 20, 0) : 1.0;
+            const bool on = t >= off;
+            n11 = on ? d11 * sc : n11;
+            n12 = on ? d12 * sc : n12;
+            n21 = on ? d21 * sc : n21;
+            n22 = on ? d22 * sc : n22;
         }
     }
     // Pq_{t-1} = n/d of the product up to pair t-1 (applied to (0, 1))
@@ -651,9 +652,10 @@ __device__ __forceinline__ int reduced_scan(double yF, double aF, double bF, dou
     for (int off = 1; off < L; off <<= 1) {
         const double pa = __shfl_up_sync(FULL, al, off, L);
         const double pb = __shfl_up_sync(FULL, be, off, L);
-        if (t >= off) {
-            be = fma(al, pb, be);
-            al *= pa;
+        {
+            const bool on = t >= off;
+            be = on ? fma(al, pb, be) : be;
+            al = on ? al * pa : al;
         }
     }
     double Pp0 = __shfl_up_sync(FULL, be, 1, L);  // Pp_{t-1}
@@ -666,9 +668,10 @@ __device__ __forceinline__ int reduced_scan(double yF, double aF, double bF, dou
     for (int off = 1; off < L; off <<= 1) {  // q_t = Qc_t + Qd_t q_{t+1}, q_{S-1} = 0
         const double c2 = __shfl_down_sync(FULL, c, off, L);
         const double g2 = __shfl_down_sync(FULL, g, off, L);
-        if (t + off < L) {
-            c = fma(g, c2, c);
-            g *= g2;
+        {
+            const bool on = t + off < L;
+            c = on ? fma(g, c2, c) : c;
+            g = on ? g * g2 : g;
         }
     }
     double qn = __shfl_down_sync(FULL, c, 1, L);
