@@ -2774,10 +2774,9 @@ k_plane(BatchView v, int s) {
             for (int off = 1; off < LY; off <<= 1) {
                 const double pa = __shfl_up_sync(FULL, fa, off, LY);
                 const double pb2 = __shfl_up_sync(FULL, fb, off, LY);
-                if (sy >= off) {
-                    fb = fma(fa, pb2, fb);
-                    fa *= pa;
-                }
+                const bool on = sy >= off;  // selects: the levels schedule as one block
+                fb = on ? fma(fa, pb2, fb) : fb;
+                fa = on ? fa * pa : fa;
             }
             double cin = __shfl_up_sync(FULL, fb, 1, LY);
             if (sy == 0) cin = 0.0;
@@ -2806,10 +2805,9 @@ k_plane(BatchView v, int s) {
             for (int off = 1; off < LY; off <<= 1) {  // x_first of every segment: suffix scan
                 const double na = __shfl_down_sync(FULL, ba, off, LY);
                 const double nb = __shfl_down_sync(FULL, bb, off, LY);
-                if (sy + off < LY) {
-                    bb = fma(ba, nb, bb);
-                    ba *= na;
-                }
+                const bool on = sy + off < LY;
+                bb = on ? fma(ba, nb, bb) : bb;
+                ba = on ? ba * na : ba;
             }
             right = __shfl_down_sync(FULL, bb, 1, LY);  // x_{a+16}; its multipliers are applied below
             if (sy == LY - 1 || !solve) right = 0.0;
